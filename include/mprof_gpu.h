@@ -1,0 +1,137 @@
+/*
+ * mprof_gpu.h — C ABI of the B200 matrix-profile join (libmprof_b200.so).
+ *
+ * This is the drop-in boundary under the reference's C++ API. Each entry point
+ * names the reference interface it replaces (paths under
+ * /root/reference/proj/include/mprof/):
+ *
+ *   mpgpu_join / mpgpu_join_timed  <- mprof::stomp   (profile.hpp:80-83)
+ *                                     mprof::scrimp  (profile.hpp:85-89, full run)
+ *   mpgpu_zone_size                <- mprof::zone_size (distance.hpp:19-20)
+ *   mpgpu_rolling_stats            <- mprof::rolling_mean_std (rolling.hpp:25-29)
+ *                                     + is_flat_std (rolling.hpp:21-23)
+ *   mpgpu_plan_*                   <- the stomp worker-chunk contract
+ *                                     (SPEC.md:267): device-resident inputs,
+ *                                     sharded diagonal work and a min-merge of
+ *                                     packed (score, index) keys, for callers
+ *                                     that own the collective (torch.distributed
+ *                                     / NCCL over NVLink).
+ *
+ * Conventions: plain pointers and sizes only; no exceptions cross the ABI;
+ * host buffers are caller-owned; the library owns device scratch, streams and
+ * peer mappings. Every call is re-entrant; calls on one device are serialised.
+ * Error text for the calling thread: mpgpu_last_error().
+ */
+#ifndef MPROF_GPU_H
+#define MPROF_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MPGPU_OK = 0,
+  MPGPU_EPARAM = 2,       /* ParameterError (error.hpp:9-13)                    */
+  MPGPU_EUNSUPPORTED = 3, /* UnsupportedError (error.hpp:15-19)                 */
+  MPGPU_ECUDA = 10,       /* CUDA runtime failure (no reference equivalent)     */
+  MPGPU_ENOMEM = 12       /* device allocation failed                           */
+} mpgpu_status;
+
+/* Host-buffer join (the reference call shape). b == NULL selects a self-join;
+ * zone is the RESOLVED half-width (mpgpu_zone_size), forced to 0 for AB-joins
+ * (SPEC.md:268). Outputs have length n_a - window + 1 (mp_b/pi_b: n_b - window
+ * + 1) and may be NULL when not wanted; left/right are self-join only.
+ * Excluded / undefined entries are +inf and -1. */
+typedef struct {
+  const double *a;
+  int64_t n_a;
+  const double *b; /* NULL -> self-join */
+  int64_t n_b;
+  int64_t window;
+  int64_t zone;
+  int32_t n_gpus;          /* <= 0 -> 1                                       */
+  const int32_t *devices;  /* NULL -> 0 .. n_gpus-1                            */
+  double *mp_a;            /* values (profile.hpp:30)                          */
+  int64_t *pi_a;           /* index (profile.hpp:31)                           */
+  int64_t *left_a;         /* left_index, self-join only (profile.hpp:32)      */
+  int64_t *right_a;        /* right_index, self-join only (profile.hpp:33)     */
+  double *mp_b;            /* AB-join: B against A from the same pass          */
+  int64_t *pi_b;
+  void (*progress)(double fraction, void *ctx); /* ProgressFn (profile.hpp:23-24) */
+  void *progress_ctx;
+} mpgpu_join_args;
+
+mpgpu_status mpgpu_join(const mpgpu_join_args *args);
+
+/* As mpgpu_join; also reports the device time of the join kernels
+ * (stats + diagonal tiles + finalize, max over devices) and the wall time of
+ * the whole call including host<->device copies, in milliseconds. */
+mpgpu_status mpgpu_join_timed(const mpgpu_join_args *args, double *kernel_ms, double *total_ms);
+
+/* Thread-local description of the last failure on this thread. */
+const char *mpgpu_last_error(void);
+
+/* round-half-up(window * fraction); -1 for a negative fraction. */
+int64_t mpgpu_zone_size(int64_t window, double fraction);
+
+/* Number of unique cells a join evaluates: (L - zone - 1)(L - zone)/2 for a
+ * self-join, L_a * L_b for an AB-join (BASELINE.md §2 unit of work). */
+int64_t mpgpu_join_cells(int64_t n_a, int64_t n_b, int64_t window, int64_t zone);
+
+/* Rolling mean / population std of every window of a DEVICE series (flat
+ * windows -> std 0 exactly). d_means / d_stds: device, length n - window + 1. */
+mpgpu_status mpgpu_rolling_stats(const double *d_ts, int64_t n, int64_t window, double *d_means,
+                                 double *d_stds, int32_t device, void *cuda_stream);
+
+/* ---- device-resident plan (sharded execution) --------------------------- */
+
+typedef struct mpgpu_plan mpgpu_plan;
+
+/* d_a / d_b: device series on `device` (caller-owned, must outlive the plan);
+ * d_b == NULL -> self-join. cuda_stream == NULL -> the plan's own stream. */
+mpgpu_plan *mpgpu_plan_create(const double *d_a, int64_t n_a, const double *d_b, int64_t n_b,
+                              int64_t window, int64_t zone, int32_t device, void *cuda_stream);
+void mpgpu_plan_destroy(mpgpu_plan *plan);
+
+/* Window statistics + flat-window index, and reset the packed keys. */
+mpgpu_status mpgpu_plan_prepare(mpgpu_plan *plan);
+
+/* Evaluate shard `shard` of `n_shards` (equal-cell contiguous ranges of the
+ * diagonal work items) into the plan's keys. Shards of one plan may run in
+ * any order; the result after all shards is bit-identical to n_shards = 1. */
+mpgpu_status mpgpu_plan_run(mpgpu_plan *plan, int32_t shard, int32_t n_shards);
+
+/* Cells evaluated by one shard (n_shards = 1: the whole join). */
+int64_t mpgpu_plan_shard_cells(const mpgpu_plan *plan, int32_t shard, int32_t n_shards);
+
+/* Device pointers to the packed int64 keys, (score bits | index), min-merged:
+ * row keys (self: right neighbours; AB: A-profile) and column keys
+ * (self: left neighbours; AB: B-profile). An element-wise MIN across shards
+ * (ncclMin / torch ReduceOp.MIN on int64) is the whole collective. */
+mpgpu_status mpgpu_plan_keys(mpgpu_plan *plan, int64_t **d_row_keys, int64_t *row_len,
+                             int64_t **d_col_keys, int64_t *col_len);
+
+/* Decode keys into the MatrixProfile arrays (device pointers, may be NULL). */
+mpgpu_status mpgpu_plan_finalize(mpgpu_plan *plan, double *d_mp_a, int64_t *d_pi_a,
+                                 int64_t *d_left_a, int64_t *d_right_a, double *d_mp_b,
+                                 int64_t *d_pi_b);
+
+/* Element-wise min of `src` into `dst` (device, same device), for merging
+ * shard keys without NCCL. */
+mpgpu_status mpgpu_keys_min_merge(int64_t *d_dst, const int64_t *d_src, int64_t len,
+                                  int32_t device, void *cuda_stream);
+
+/* Kernel launches issued by the last plan_prepare + plan_run + plan_finalize
+ * sequence on this plan (for bench accounting). */
+int64_t mpgpu_plan_launch_count(const mpgpu_plan *plan);
+
+/* Library build string (arch, tile shape). */
+const char *mpgpu_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,194 @@
+"""CPU ORACLE — TEST INFRASTRUCTURE ONLY.
+
+ctypes wrapper over ``oracle/liboracle.so`` (a plain-C restatement of the
+reference hot path, see ``mprof_oracle.h``) and ``oracle/_ref/libref_types.so``
+(the reference's own ``TimeSeries`` constructor, compiled from
+/root/reference/proj/src/types.cpp by ``oracle/Makefile``).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU baseline /
+``--impl reference`` arm may import this package. The product package
+``paper_1904_12626_b200`` never imports it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liboracle.so")
+_REF_LIB = os.path.join(_HERE, "_ref", "libref_types.so")
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int64)
+_lib = None
+_ref = None
+
+
+def build() -> None:
+    """Compile liboracle.so (and _ref/ when the reference tree is present)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            build()
+        lib = ctypes.CDLL(_LIB)
+        lib.or_zone_size.restype = ctypes.c_int64
+        lib.or_zone_size.argtypes = [ctypes.c_int64, ctypes.c_double]
+        lib.or_is_flat_std.restype = ctypes.c_int
+        lib.or_is_flat_std.argtypes = [ctypes.c_double, ctypes.c_double]
+        lib.or_rolling_mean_std.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, _dp, _dp, ctypes.c_int]
+        lib.or_znorm_dist_from_qt.restype = ctypes.c_double
+        lib.or_znorm_dist_from_qt.argtypes = [ctypes.c_double, ctypes.c_int64] + [ctypes.c_double] * 4
+        lib.or_sliding_dot_direct.argtypes = [_dp, ctypes.c_int64, _dp, ctypes.c_int64, _dp]
+        lib.or_brute_force_mp.argtypes = [_dp, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_double, _dp, _ip, _ip, _ip, ctypes.c_int]
+        lib.or_brute_force_rows.argtypes = [_dp, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64,
+                                            ctypes.c_double, _ip, ctypes.c_int64, _dp, _ip, _ip, _ip,
+                                            ctypes.c_int]
+        lib.or_stomp.argtypes = [_dp, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                 ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _dp, _ip, _ip, _ip]
+        lib.or_scrimp.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
+                                  ctypes.c_uint64, _dp, _ip, _ip, _ip, _dp]
+        lib.or_merge_min.restype = None
+        lib.or_merge_min.argtypes = [_dp, _ip, _dp, ctypes.c_int64, ctypes.c_int64]
+        _lib = lib
+    return _lib
+
+
+def _d(x):
+    return x.ctypes.data_as(_dp) if x is not None else None
+
+
+def _i(x):
+    return x.ctypes.data_as(_ip) if x is not None else None
+
+
+def _f64(x):
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def default_threads() -> int:
+    return max(1, len(os.sched_getaffinity(0)))
+
+
+def zone_size(window: int, fraction: float) -> int:
+    z = _load().or_zone_size(int(window), float(fraction))
+    if z < 0:
+        raise ValueError("negative exclusion-zone fraction")
+    return int(z)
+
+
+def is_flat_std(sd: float, mean: float) -> bool:
+    return bool(_load().or_is_flat_std(float(sd), float(mean)))
+
+
+def rolling_mean_std(ts, w: int, threads: int = 1):
+    ts = _f64(ts)
+    L = ts.size - w + 1
+    if w < 4 or L < 1:
+        raise ValueError("window out of range")
+    mu = np.empty(L)
+    sd = np.empty(L)
+    if _load().or_rolling_mean_std(_d(ts), ts.size, w, _d(mu), _d(sd), threads):
+        raise ValueError("window out of range")
+    return mu, sd
+
+
+def znorm_dist_from_qt(qt, w, mu_a, sd_a, mu_b, sd_b) -> float:
+    return float(_load().or_znorm_dist_from_qt(qt, w, mu_a, sd_a, mu_b, sd_b))
+
+
+def sliding_dot_direct(q, ts):
+    q, ts = _f64(q), _f64(ts)
+    out = np.empty(ts.size - q.size + 1)
+    if _load().or_sliding_dot_direct(_d(q), q.size, _d(ts), ts.size, _d(out)):
+        raise ValueError("length mismatch")
+    return out
+
+
+def _alloc(L, lr=True):
+    return (np.empty(L), np.empty(L, np.int64), np.empty(L, np.int64) if lr else None,
+            np.empty(L, np.int64) if lr else None)
+
+
+def brute_force_mp(a, b=None, w=4, ez=0.5, threads=None):
+    """brute_force_mp (profile.hpp:70-73). Returns (mp, pi, left, right)."""
+    a = _f64(a)
+    bb = _f64(b) if b is not None else None
+    La = a.size - w + 1
+    mp, pi, le, ri = _alloc(La, b is None)
+    rc = _load().or_brute_force_mp(_d(a), a.size, _d(bb), 0 if bb is None else bb.size, w, ez,
+                                   _d(mp), _i(pi), _i(le), _i(ri), threads or default_threads())
+    if rc:
+        raise ValueError("invalid window / fraction")
+    return mp, pi, le, ri
+
+
+def brute_force_rows(a, rows, b=None, w=4, ez=0.5, threads=None):
+    """Exact MP / PI / left / right at the given profile positions only."""
+    a = _f64(a)
+    bb = _f64(b) if b is not None else None
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    mp, pi, le, ri = _alloc(rows.size, b is None)
+    rc = _load().or_brute_force_rows(_d(a), a.size, _d(bb), 0 if bb is None else bb.size, w, ez,
+                                     _i(rows), rows.size, _d(mp), _i(pi), _i(le), _i(ri),
+                                     threads or default_threads())
+    if rc:
+        raise ValueError("invalid rows / window")
+    return mp, pi, le, ri
+
+
+def stomp(a, b=None, w=4, ez=0.5, n_workers=1, row_begin=0, row_end=0):
+    """stomp (profile.hpp:80-83). Returns (mp, pi, left, right) for the A-profile."""
+    a = _f64(a)
+    bb = _f64(b) if b is not None else None
+    La = a.size - w + 1
+    mp, pi, le, ri = _alloc(La, True)
+    rc = _load().or_stomp(_d(a), a.size, _d(bb), 0 if bb is None else bb.size, w, ez, int(n_workers),
+                          int(row_begin), int(row_end), _d(mp), _i(pi), _i(le), _i(ri))
+    if rc:
+        raise ValueError("invalid window / fraction")
+    if b is not None:
+        le = ri = None
+    return mp, pi, le, ri
+
+
+def scrimp(a, w=4, ez=0.5, s_size=0, seed=0):
+    """scrimp (profile.hpp:85-89). Returns (mp, pi, left, right, coverage)."""
+    a = _f64(a)
+    La = a.size - w + 1
+    mp, pi, le, ri = _alloc(La, True)
+    cov = ctypes.c_double(0)
+    rc = _load().or_scrimp(_d(a), a.size, w, ez, int(s_size), ctypes.c_uint64(seed), _d(mp), _i(pi),
+                           _i(le), _i(ri), ctypes.byref(cov))
+    if rc:
+        raise ValueError("invalid window / fraction")
+    return mp, pi, le, ri, cov.value
+
+
+def merge_min(acc, acc_idx, dp, source_index):
+    _load().or_merge_min(_d(acc), _i(acc_idx), _d(_f64(dp)), acc.size, int(source_index))
+
+
+def ref_timeseries_validate(x):
+    """Run the reference's own TimeSeries constructor (types.cpp:7-18).
+
+    Returns (code, message): 0 = accepted, 2 = ParameterError. Raises
+    FileNotFoundError when oracle/_ref was never built.
+    """
+    global _ref
+    if _ref is None:
+        if not os.path.exists(_REF_LIB):
+            raise FileNotFoundError(_REF_LIB)
+        _ref = ctypes.CDLL(_REF_LIB)
+        _ref.ref_timeseries_validate.argtypes = [_dp, ctypes.c_int64, ctypes.c_char_p, ctypes.c_int]
+    x = _f64(x)
+    buf = ctypes.create_string_buffer(256)
+    rc = _ref.ref_timeseries_validate(_d(x), x.size, buf, 256)
+    return rc, buf.value.decode()

@@ -1,0 +1,413 @@
+"""B200-native exact z-normalised similarity join (matrix profile).
+
+Python mirror of the reference's C++ hot-path API
+(/root/reference/proj/include/mprof/profile.hpp:80-89): ``stomp`` and
+``scrimp`` take a series, a window and an exclusion-zone fraction and return a
+``MatrixProfile`` with the reference's fields and error behaviour
+(ParameterError / UnsupportedError, error.hpp:9-19). Everything runs through
+the C ABI of ``libmprof_b200.so`` (include/mprof_gpu.h) on sm_100a; there is
+no CPU fallback — a missing library or GPU raises.
+
+``Plan`` exposes the device-resident, sharded form (torch CUDA tensors in,
+packed int64 keys out) that ``bench.py`` drives across ranks with
+``torch.distributed`` (NCCL ReduceOp.MIN over the keys).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "ParameterError", "UnsupportedError", "MatrixProfile", "zone_size", "join_cells",
+    "stomp", "scrimp", "stomp_ab", "join", "Plan", "rolling_stats", "lib", "K_FULL_RUN",
+    "MIN_WINDOW",
+]
+
+K_FULL_RUN = (1 << 63) - 1   # kFullRun (profile.hpp:20-21)
+MIN_WINDOW = 4               # kMinWindow (types.hpp:19-21)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libmprof_b200.so")
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_ip = ctypes.POINTER(ctypes.c_int64)
+_PROGRESS = ctypes.CFUNCTYPE(None, ctypes.c_double, ctypes.c_void_p)
+
+MPGPU_OK, MPGPU_EPARAM, MPGPU_EUNSUPPORTED = 0, 2, 3
+
+
+class ParameterError(ValueError):
+    """Invalid argument (reference ParameterError, error.hpp:9-13)."""
+
+
+class UnsupportedError(ParameterError):
+    """Unsupported mode combination (reference UnsupportedError, error.hpp:15-19)."""
+
+
+class _JoinArgs(ctypes.Structure):
+    _fields_ = [
+        ("a", _dp), ("n_a", ctypes.c_int64), ("b", _dp), ("n_b", ctypes.c_int64),
+        ("window", ctypes.c_int64), ("zone", ctypes.c_int64),
+        ("n_gpus", ctypes.c_int32), ("devices", ctypes.POINTER(ctypes.c_int32)),
+        ("mp_a", _dp), ("pi_a", _ip), ("left_a", _ip), ("right_a", _ip),
+        ("mp_b", _dp), ("pi_b", _ip),
+        ("progress", _PROGRESS), ("progress_ctx", ctypes.c_void_p),
+    ]
+
+
+def lib() -> ctypes.CDLL:
+    """Load libmprof_b200.so (built in-tree by build.py). Raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(
+            f"{_LIB_PATH} is missing: run `python -m paper_1904_12626_b200.build` "
+            "(the product has no CPU fallback)")
+    L = ctypes.CDLL(_LIB_PATH)
+    L.mpgpu_join.argtypes = [ctypes.POINTER(_JoinArgs)]
+    L.mpgpu_join.restype = ctypes.c_int
+    L.mpgpu_join_timed.argtypes = [ctypes.POINTER(_JoinArgs), _dp, _dp]
+    L.mpgpu_join_timed.restype = ctypes.c_int
+    L.mpgpu_last_error.restype = ctypes.c_char_p
+    L.mpgpu_zone_size.argtypes = [ctypes.c_int64, ctypes.c_double]
+    L.mpgpu_zone_size.restype = ctypes.c_int64
+    L.mpgpu_join_cells.argtypes = [ctypes.c_int64] * 4
+    L.mpgpu_join_cells.restype = ctypes.c_int64
+    L.mpgpu_rolling_stats.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                      ctypes.c_void_p]
+    L.mpgpu_rolling_stats.restype = ctypes.c_int
+    L.mpgpu_plan_create.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]
+    L.mpgpu_plan_create.restype = ctypes.c_void_p
+    L.mpgpu_plan_destroy.argtypes = [ctypes.c_void_p]
+    L.mpgpu_plan_destroy.restype = None
+    L.mpgpu_plan_prepare.argtypes = [ctypes.c_void_p]
+    L.mpgpu_plan_prepare.restype = ctypes.c_int
+    L.mpgpu_plan_run.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
+    L.mpgpu_plan_run.restype = ctypes.c_int
+    L.mpgpu_plan_shard_cells.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
+    L.mpgpu_plan_shard_cells.restype = ctypes.c_int64
+    L.mpgpu_plan_keys.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), _ip,
+                                  ctypes.POINTER(ctypes.c_void_p), _ip]
+    L.mpgpu_plan_keys.restype = ctypes.c_int
+    L.mpgpu_plan_finalize.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 6
+    L.mpgpu_plan_finalize.restype = ctypes.c_int
+    L.mpgpu_keys_min_merge.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                       ctypes.c_int32, ctypes.c_void_p]
+    L.mpgpu_keys_min_merge.restype = ctypes.c_int
+    L.mpgpu_plan_launch_count.argtypes = [ctypes.c_void_p]
+    L.mpgpu_plan_launch_count.restype = ctypes.c_int64
+    L.mpgpu_build_info.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(status: int) -> None:
+    if status == MPGPU_OK:
+        return
+    msg = lib().mpgpu_last_error().decode(errors="replace")
+    if status == MPGPU_EUNSUPPORTED:
+        raise UnsupportedError(msg)
+    if status == MPGPU_EPARAM:
+        raise ParameterError(msg)
+    raise RuntimeError(f"mprof_b200 error {status}: {msg}")
+
+
+# --------------------------------------------------------------------- results
+@dataclass
+class MatrixProfile:
+    """Mirror of mprof::MatrixProfile (profile.hpp:28-46)."""
+    values: np.ndarray
+    index: np.ndarray
+    left_index: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    right_index: np.ndarray = field(default_factory=lambda: np.empty(0, np.int64))
+    window: int = 0
+    exclusion_zone: int = 0
+    mode: str = "stomp"
+    join_kind: str = "self"
+    coverage: float = 1.0
+    seed: int = 0
+    data_len: int = 0
+    data_len_b: int = 0
+    data_dims: int = 1
+
+    def size(self) -> int:
+        return int(self.values.size)
+
+    def full_coverage(self) -> bool:
+        return self.coverage >= 1.0
+
+    def has_left_right(self) -> bool:
+        return self.left_index.size > 0
+
+
+# --------------------------------------------------------------------- helpers
+def _series(x, name: str) -> np.ndarray:
+    """TimeSeries validation (types.cpp:7-18): length >= 4, all finite."""
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64).ravel())
+    if a.size < MIN_WINDOW:
+        raise ParameterError(f"time series too short: length {a.size} < minimum {MIN_WINDOW}")
+    bad = np.flatnonzero(~np.isfinite(a))
+    if bad.size:
+        raise ParameterError(f"time series sample {int(bad[0])} is not finite")
+    return a
+
+
+def _check_window(w: int, n: int, what: str) -> None:
+    if w < MIN_WINDOW:
+        raise ParameterError(f"window {w} < minimum {MIN_WINDOW}")
+    if w > n:
+        raise ParameterError(f"window {w} exceeds {what} length {n}")
+
+
+def zone_size(window: int, fraction: float) -> int:
+    """round-half-up(window * fraction) (distance.hpp:19-20)."""
+    if not (fraction >= 0.0):
+        raise ParameterError("exclusion-zone fraction must be >= 0")
+    return int(lib().mpgpu_zone_size(int(window), float(fraction)))
+
+
+def join_cells(n_a: int, n_b: int, window: int, zone: int) -> int:
+    """Unique cells of a join (self-join when n_b == 0)."""
+    return int(lib().mpgpu_join_cells(int(n_a), int(n_b), int(window), int(zone)))
+
+
+def _ptr(a: Optional[np.ndarray], typ):
+    return a.ctypes.data_as(typ) if a is not None else None
+
+
+def join(a, b=None, window: int = 4, zone: int = 0, *, n_gpus: int = 1,
+         devices: Optional[Sequence[int]] = None, want_b: bool = True,
+         progress: Optional[Callable[[float], None]] = None, timed: bool = False):
+    """Raw host-buffer join through ``mpgpu_join`` (zone already resolved).
+
+    Returns a dict with mp_a, pi_a (+ left_a, right_a for self-joins; mp_b,
+    pi_b for AB-joins) and, when ``timed``, kernel_ms / total_ms.
+    """
+    A = _series(a, "series")
+    B = _series(b, "series B") if b is not None else None
+    _check_window(window, A.size, "series")
+    if B is not None:
+        _check_window(window, B.size, "series B")
+    La = A.size - window + 1
+    out = {"mp_a": np.empty(La), "pi_a": np.empty(La, np.int64)}
+    args = _JoinArgs()
+    args.a = _ptr(A, _dp)
+    args.n_a = A.size
+    args.b = _ptr(B, _dp)
+    args.n_b = 0 if B is None else B.size
+    args.window = int(window)
+    args.zone = int(zone) if B is None else 0
+    args.n_gpus = int(n_gpus)
+    dev_arr = None
+    if devices is not None:
+        dev_arr = (ctypes.c_int32 * len(devices))(*devices)
+        args.devices = ctypes.cast(dev_arr, ctypes.POINTER(ctypes.c_int32))
+        args.n_gpus = len(devices)
+    args.mp_a = _ptr(out["mp_a"], _dp)
+    args.pi_a = _ptr(out["pi_a"], _ip)
+    if B is None:
+        out["left_a"] = np.empty(La, np.int64)
+        out["right_a"] = np.empty(La, np.int64)
+        args.left_a = _ptr(out["left_a"], _ip)
+        args.right_a = _ptr(out["right_a"], _ip)
+    elif want_b:
+        Lb = B.size - window + 1
+        out["mp_b"] = np.empty(Lb)
+        out["pi_b"] = np.empty(Lb, np.int64)
+        args.mp_b = _ptr(out["mp_b"], _dp)
+        args.pi_b = _ptr(out["pi_b"], _ip)
+    cb = None
+    if progress is not None:
+        cb = _PROGRESS(lambda f, _ctx: progress(f))
+        args.progress = cb
+    if timed:
+        k = ctypes.c_double(0)
+        t = ctypes.c_double(0)
+        _check(lib().mpgpu_join_timed(ctypes.byref(args), ctypes.byref(k), ctypes.byref(t)))
+        out["kernel_ms"], out["total_ms"] = k.value, t.value
+    else:
+        _check(lib().mpgpu_join(ctypes.byref(args)))
+    del dev_arr, cb
+    return out
+
+
+def stomp(ts_a, ts_b=None, window: int = 4, ez_fraction: float = 0.5, n_workers: int = 1,
+          progress: Optional[Callable[[float], None]] = None, *, n_gpus: int = 1,
+          devices: Optional[Sequence[int]] = None) -> MatrixProfile:
+    """mprof::stomp (profile.hpp:80-83) on the B200. ts_b None -> self-join."""
+    if n_workers < 1:
+        raise ParameterError("n_workers must be >= 1")
+    A = _series(ts_a, "series")
+    B = _series(ts_b, "series B") if ts_b is not None else None
+    _check_window(window, A.size, "series")
+    if B is not None:
+        _check_window(window, B.size, "series B")
+    zone = zone_size(window, ez_fraction)
+    r = join(A, B, window, zone, n_gpus=n_gpus, devices=devices, want_b=False, progress=progress)
+    mp = MatrixProfile(values=r["mp_a"], index=r["pi_a"], window=window, mode="stomp",
+                       data_len=A.size)
+    if B is None:
+        mp.left_index, mp.right_index = r["left_a"], r["right_a"]
+        mp.exclusion_zone = zone
+    else:
+        mp.join_kind = "ab"
+        mp.data_len_b = B.size
+    return mp
+
+
+def stomp_ab(ts_a, ts_b, window: int, *, n_gpus: int = 1):
+    """Both AB-join profiles from one pass: (A against B, B against A)."""
+    A, B = _series(ts_a, "series"), _series(ts_b, "series B")
+    _check_window(window, A.size, "series")
+    _check_window(window, B.size, "series B")
+    r = join(A, B, window, 0, n_gpus=n_gpus, want_b=True)
+    pa = MatrixProfile(values=r["mp_a"], index=r["pi_a"], window=window, join_kind="ab",
+                       data_len=A.size, data_len_b=B.size)
+    pb = MatrixProfile(values=r["mp_b"], index=r["pi_b"], window=window, join_kind="ab",
+                       data_len=B.size, data_len_b=A.size)
+    return pa, pb
+
+
+def scrimp(ts_a, window: int = 4, ez_fraction: float = 0.5, s_size: int = K_FULL_RUN,
+           seed: int = 0, progress: Optional[Callable[[float], None]] = None,
+           ts_b=None) -> MatrixProfile:
+    """mprof::scrimp (profile.hpp:85-89), full coverage, self-join only.
+
+    An AB-join raises UnsupportedError; an anytime partial run
+    (s_size below the number of diagonals) raises UnsupportedError too — the
+    B200 backend computes the full join, which is what kFullRun asks for.
+    """
+    if ts_b is not None:
+        raise UnsupportedError("SCRIMP supports self-joins only")
+    if s_size < 1:
+        raise ParameterError("s_size must be >= 1")
+    A = _series(ts_a, "series")
+    _check_window(window, A.size, "series")
+    zone = zone_size(window, ez_fraction)
+    n_diag = max(0, A.size - window + 1 - zone - 1)
+    if s_size < n_diag:
+        raise UnsupportedError("anytime SCRIMP (s_size < number of diagonals) is not provided "
+                               "by the B200 backend; pass K_FULL_RUN")
+    r = join(A, None, window, zone, progress=progress)
+    return MatrixProfile(values=r["mp_a"], index=r["pi_a"], left_index=r["left_a"],
+                         right_index=r["right_a"], window=window, exclusion_zone=zone,
+                         mode="scrimp", seed=seed, data_len=A.size)
+
+
+# --------------------------------------------------------------- device plans
+class _CudaArray:
+    """__cuda_array_interface__ view of a library-owned device buffer."""
+
+    def __init__(self, ptr: int, n: int, typestr: str, owner):
+        self.__cuda_array_interface__ = {
+            "shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3, "strides": None,
+        }
+        self._owner = owner
+
+
+def _dev_ptr(t) -> int:
+    if t is None:
+        return 0
+    if not t.is_cuda or not t.is_contiguous():
+        raise ParameterError("expected a contiguous CUDA tensor")
+    return int(t.data_ptr())
+
+
+class Plan:
+    """Device-resident join over torch CUDA float64 tensors (mpgpu_plan_*)."""
+
+    def __init__(self, a, b=None, window: int = 4, zone: int = 0, stream=None):
+        import torch  # plumbing only: device memory and streams
+        if a.dtype != torch.float64 or (b is not None and b.dtype != torch.float64):
+            raise ParameterError("series must be float64")
+        _check_window(window, a.numel(), "series")
+        if b is not None:
+            _check_window(window, b.numel(), "series B")
+        self.a, self.b = a, b
+        self.window = int(window)
+        self.self_join = b is None
+        self.zone = int(zone) if b is None else 0
+        self.device = a.device.index if a.device.index is not None else torch.cuda.current_device()
+        self.stream = stream if stream is not None else torch.cuda.current_stream(a.device)
+        self.La = a.numel() - window + 1
+        self.Lb = self.La if b is None else b.numel() - window + 1
+        p = lib().mpgpu_plan_create(_dev_ptr(a), a.numel(), _dev_ptr(b) or None,
+                                    0 if b is None else b.numel(), self.window, self.zone,
+                                    self.device, ctypes.c_void_p(self.stream.cuda_stream))
+        if not p:
+            _check(MPGPU_EPARAM if b is not None or window >= MIN_WINDOW else 10)
+            raise RuntimeError(lib().mpgpu_last_error().decode())
+        self._p = ctypes.c_void_p(p)
+
+    def close(self) -> None:
+        if getattr(self, "_p", None):
+            lib().mpgpu_plan_destroy(self._p)
+            self._p = None
+
+    __del__ = close
+
+    def prepare(self) -> None:
+        _check(lib().mpgpu_plan_prepare(self._p))
+
+    def run(self, shard: int = 0, n_shards: int = 1) -> None:
+        _check(lib().mpgpu_plan_run(self._p, int(shard), int(n_shards)))
+
+    def cells(self, shard: int = 0, n_shards: int = 1) -> int:
+        return int(lib().mpgpu_plan_shard_cells(self._p, int(shard), int(n_shards)))
+
+    def launches(self) -> int:
+        return int(lib().mpgpu_plan_launch_count(self._p))
+
+    def keys(self):
+        """(row_keys, col_keys) as int64 CUDA tensors aliasing the plan's keys."""
+        import torch
+        pr, pc = ctypes.c_void_p(), ctypes.c_void_p()
+        lr, lc = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().mpgpu_plan_keys(self._p, ctypes.byref(pr), ctypes.byref(lr), ctypes.byref(pc),
+                                     ctypes.byref(lc)))
+        dev = torch.device("cuda", self.device)
+        r = torch.as_tensor(_CudaArray(pr.value, lr.value, "<i8", self), device=dev)
+        c = torch.as_tensor(_CudaArray(pc.value, lc.value, "<i8", self), device=dev)
+        return r, c
+
+    def finalize(self, mp_a=None, pi_a=None, left_a=None, right_a=None, mp_b=None, pi_b=None):
+        _check(lib().mpgpu_plan_finalize(self._p, *[ctypes.c_void_p(_dev_ptr(t) or None)
+                                                     for t in (mp_a, pi_a, left_a, right_a, mp_b, pi_b)]))
+
+    def outputs(self):
+        """Allocate and fill the MatrixProfile arrays on the device."""
+        import torch
+        dev = self.a.device
+        o = {"mp_a": torch.empty(self.La, dtype=torch.float64, device=dev),
+             "pi_a": torch.empty(self.La, dtype=torch.int64, device=dev)}
+        if self.self_join:
+            o["left_a"] = torch.empty(self.La, dtype=torch.int64, device=dev)
+            o["right_a"] = torch.empty(self.La, dtype=torch.int64, device=dev)
+        else:
+            o["mp_b"] = torch.empty(self.Lb, dtype=torch.float64, device=dev)
+            o["pi_b"] = torch.empty(self.Lb, dtype=torch.int64, device=dev)
+        self.finalize(o["mp_a"], o["pi_a"], o.get("left_a"), o.get("right_a"), o.get("mp_b"),
+                      o.get("pi_b"))
+        return o
+
+
+def rolling_stats(ts, window: int, stream=None):
+    """rolling_mean_std (rolling.hpp:25-29) of a float64 CUDA tensor."""
+    import torch
+    _check_window(window, ts.numel(), "series")
+    L = ts.numel() - window + 1
+    mu = torch.empty(L, dtype=torch.float64, device=ts.device)
+    sd = torch.empty(L, dtype=torch.float64, device=ts.device)
+    st = stream if stream is not None else torch.cuda.current_stream(ts.device)
+    _check(lib().mpgpu_rolling_stats(_dev_ptr(ts), ts.numel(), int(window), _dev_ptr(mu),
+                                     _dev_ptr(sd), ts.device.index or 0,
+                                     ctypes.c_void_p(st.cuda_stream)))
+    return mu, sd

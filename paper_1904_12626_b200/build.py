@@ -1,0 +1,56 @@
+"""Build libmprof_b200.so in-tree (nvcc, sm_100a) — no JIT cache, no pip install."""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libmprof_b200.so")
+SOURCES = ["mpgpu.cu", "mprof_api.cpp"]
+HEADERS = ["mpgpu_kernels.cuh"]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def needs_build() -> bool:
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps += [os.path.join(ROOT, "include", "mprof_gpu.h")]
+    deps += [os.path.join(ROOT, "include", "mprof", f) for f in os.listdir(os.path.join(ROOT, "include", "mprof"))]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not needs_build():
+        return OUT
+    cmd = [
+        _nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
+        "-std=c++20", "-Xcompiler", "-fPIC,-O3", "-shared", "-Xptxas", "-v",
+        "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
+        *[os.path.join(CSRC, s) for s in SOURCES], "-o", OUT + ".tmp",
+    ]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libmprof_b200.so")
+    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+        f.write(r.stderr)
+    os.replace(OUT + ".tmp", OUT)
+    if verbose:
+        print(r.stderr)
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,716 @@
+// Host side of the B200 matrix-profile join: plans, work items, sharding,
+// multi-device orchestration and the C ABI declared in include/mprof_gpu.h.
+//
+// Reference boundary: mprof::stomp / mprof::scrimp (profile.hpp:80-89). The
+// C++ shim in mprof_api.cpp keeps those signatures and calls mpgpu_join.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "mprof_gpu.h"
+#include "mpgpu_kernels.cuh"
+
+using namespace mpgpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+mpgpu_status fail(mpgpu_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+#define MPG_CUDA(call)                                                                      \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? MPGPU_ENOMEM : MPGPU_ECUDA,             \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                      \
+    }                                                                                       \
+  } while (0)
+
+int ceil_log2(long long v) {
+  int b = 0;
+  while ((1LL << b) < v) ++b;
+  return b;
+}
+
+// sum_{k=k1}^{k2-1} clamp(A - k, 0, N)  (valid rows of one diagonal in a segment)
+long long sum_clamp(long long A, long long k1, long long k2, long long N) {
+  long long total = 0;
+  if (k2 <= k1 || N <= 0) return 0;
+  // region where A - k >= N : k <= A - N  -> contributes N
+  const long long kfull_hi = std::min(k2, A - N + 1);
+  if (kfull_hi > k1) total += (kfull_hi - k1) * N;
+  // region where 0 < A - k < N
+  const long long lo = std::max(k1, A - N + 1), hi = std::min(k2, A);
+  if (hi > lo) {
+    // sum_{k=lo}^{hi-1} (A - k) = sum of an arithmetic series
+    const long long first = A - lo, last = A - (hi - 1);
+    total += (first + last) * (hi - lo) / 2;
+  }
+  return total;
+}
+
+struct DevSeries {
+  double* mu = nullptr;
+  double* inv = nullptr;
+  double* sd = nullptr;
+  double2* U = nullptr;
+  uint8_t* flat = nullptr;
+  uint32_t* words = nullptr;
+  int32_t* next = nullptr;
+  long long n = 0, L = 0;
+  int n_words = 0;
+  const double* x = nullptr;
+
+  Series view() const {
+    Series s;
+    s.x = x; s.mu = mu; s.inv = inv; s.U = U; s.flat_words = words; s.next_word = next;
+    s.n = n; s.L = L; s.n_words = n_words;
+    return s;
+  }
+  void release() {
+    cudaFree(mu); cudaFree(inv); cudaFree(sd); cudaFree(U); cudaFree(flat); cudaFree(words);
+    cudaFree(next);
+    mu = inv = sd = nullptr; U = nullptr; flat = nullptr; words = nullptr; next = nullptr;
+  }
+};
+
+}  // namespace
+
+struct mpgpu_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  bool self = true;
+  long long m = 0, zone = 0;
+  int index_bits = 1;
+  long long imask = 1;
+  DevSeries A, B;
+  long long* key0 = nullptr;  // self: right (row) keys; AB: A keys
+  long long* key1 = nullptr;  // self: left (column) keys; AB: B keys
+  std::vector<Item> items;    // sorted, largest first
+  std::vector<long long> item_cells;
+  std::vector<long long> prefix;  // prefix[i] = cells of items[0..i)
+  Item* d_items = nullptr;
+  int* d_counter = nullptr;
+  int n_ctas = 0;
+  long long launches = 0;
+  long long seg_rows = 0;
+};
+
+namespace {
+
+mpgpu_status alloc_series(DevSeries& s, const double* x, long long n, long long m) {
+  s.x = x;
+  s.n = n;
+  s.L = n - m + 1;
+  s.n_words = (int)((s.L + 31) / 32);
+  MPG_CUDA(cudaMalloc(&s.mu, sizeof(double) * s.L));
+  MPG_CUDA(cudaMalloc(&s.inv, sizeof(double) * (s.L + kPad)));
+  MPG_CUDA(cudaMalloc(&s.U, sizeof(double2) * (s.L + kPad)));
+  MPG_CUDA(cudaMalloc(&s.flat, s.L));
+  MPG_CUDA(cudaMalloc(&s.words, sizeof(uint32_t) * s.n_words));
+  MPG_CUDA(cudaMalloc(&s.next, sizeof(int32_t) * s.n_words));
+  return MPGPU_OK;
+}
+
+mpgpu_status launch_stats(mpgpu_plan* p, DevSeries& s) {
+  const int bs = 256;
+  k_window_stats<<<(unsigned)((s.L + bs - 1) / bs), bs, 0, p->stream>>>(s.x, s.L, (int)p->m, s.mu,
+                                                                          s.inv, nullptr, s.flat);
+  k_update_vectors<<<(unsigned)((s.L + kPad + bs - 1) / bs), bs, 0, p->stream>>>(
+      s.x, s.mu, s.L, (int)p->m, s.U, s.inv);
+  k_flat_words<<<(unsigned)((s.n_words * 32LL + bs - 1) / bs), bs, 0, p->stream>>>(
+      s.flat, s.L, s.n_words, s.words);
+  k_next_word<<<1, 1024, 0, p->stream>>>(s.words, s.n_words, s.next);
+  p->launches += 4;
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+// Work items: for each pass, bands of kW diagonals, each cut into segments of
+// seg_rows rows (a multiple of kH). Segment length depends only on the problem
+// (never on the shard count), so results are bit-identical for any sharding.
+void build_items(mpgpu_plan* p) {
+  struct PassGeom { long long LR, LC, klo, khi; };
+  std::vector<PassGeom> geo;
+  if (p->self) {
+    geo.push_back({p->A.L, p->A.L, p->zone + 1, p->A.L});
+  } else {
+    geo.push_back({p->A.L, p->B.L, 0, p->B.L});  // rows A, cols B, k >= 0
+    geo.push_back({p->B.L, p->A.L, 1, p->A.L});  // rows B, cols A, k >= 1
+  }
+  // total cells for segment sizing
+  long long cells = 0;
+  for (auto& g : geo) {
+    if (g.khi <= g.klo) continue;
+    // sum_k min(LR, LC - k) over k in [klo, khi)
+    cells += sum_clamp(g.LC, g.klo, g.khi, g.LR);
+  }
+  const long long ref_ctas = 296;  // 148 SMs x 2 CTAs (fixed: independent of device & shards)
+  long long seg = cells / ((long long)kW * 64 * ref_ctas);
+  seg = std::max<long long>(kH, std::min<long long>(16384, seg));
+  seg = (seg / kH) * kH;
+  p->seg_rows = seg;
+
+  p->items.clear();
+  p->item_cells.clear();
+  for (int pi = 0; pi < (int)geo.size(); ++pi) {
+    const auto& g = geo[pi];
+    for (long long kb = g.klo; kb < g.khi; kb += kW) {
+      const long long ke = std::min(kb + kW, g.khi);
+      const long long rows_needed = std::min(g.LR, g.LC - kb);
+      if (rows_needed <= 0) continue;
+      for (long long r0 = 0; r0 < rows_needed; r0 += seg) {
+        const long long nr = std::min(seg, rows_needed - r0);
+        Item it;
+        it.pass = pi;
+        it.kb = kb;
+        it.r0 = r0;
+        it.nrows = (int)(((nr + kH - 1) / kH) * kH);
+        // valid cells: sum_k clamp(min(LR, LC - k) - r0, 0, nr); min() switches
+        // from LR to LC - k at k = LC - LR
+        const long long ksplit = std::min(ke, std::max(kb, g.LC - g.LR + 1));
+        const long long c = (ksplit - kb) * std::max(0LL, std::min(g.LR - r0, nr)) +
+                            sum_clamp(g.LC - r0, ksplit, ke, nr);
+        p->items.push_back(it);
+        p->item_cells.push_back(c);
+      }
+    }
+  }
+  // largest first (longest-processing-time order for the persistent queue)
+  std::vector<size_t> order(p->items.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+    return p->item_cells[a] > p->item_cells[b];
+  });
+  std::vector<Item> its(order.size());
+  std::vector<long long> cs(order.size());
+  for (size_t i = 0; i < order.size(); ++i) {
+    its[i] = p->items[order[i]];
+    cs[i] = p->item_cells[order[i]];
+  }
+  p->items.swap(its);
+  p->item_cells.swap(cs);
+  p->prefix.assign(p->items.size() + 1, 0);
+  for (size_t i = 0; i < p->items.size(); ++i) p->prefix[i + 1] = p->prefix[i] + p->item_cells[i];
+}
+
+// Items of shard s: round-robin by cost rank (item q goes to shard q % n), so
+// every shard receives the same mix of large and small items.
+void shard_items(const mpgpu_plan* p, int shard, int n_shards, std::vector<Item>& out,
+                 long long* cells) {
+  out.clear();
+  long long c = 0;
+  for (size_t q = (size_t)shard; q < p->items.size(); q += (size_t)n_shards) {
+    out.push_back(p->items[q]);
+    c += p->item_cells[q];
+  }
+  if (cells) *cells = c;
+}
+
+JoinParams make_params(const mpgpu_plan* p) {
+  JoinParams P;
+  memset(&P, 0, sizeof(P));
+  if (p->self) {
+    P.pass[0].R = p->A.view();
+    P.pass[0].C = p->A.view();
+    P.pass[0].keyR = p->key0;
+    P.pass[0].keyC = p->key1;
+  } else {
+    P.pass[0].R = p->A.view();
+    P.pass[0].C = p->B.view();
+    P.pass[0].keyR = p->key0;
+    P.pass[0].keyC = p->key1;
+    P.pass[1].R = p->B.view();
+    P.pass[1].C = p->A.view();
+    P.pass[1].keyR = p->key1;
+    P.pass[1].keyC = p->key0;
+  }
+  P.m = (int)p->m;
+  P.imask = p->imask;
+  return P;
+}
+
+std::once_flag g_attr_once;
+int g_ctas_per_sm = 0;
+
+}  // namespace
+
+extern "C" {
+
+const char* mpgpu_last_error(void) { return g_err.c_str(); }
+
+const char* mpgpu_build_info(void) {
+  static char buf[160];
+  snprintf(buf, sizeof(buf), "mprof_b200 sm_100a fp64 D=%d warps=%d W=%d H=%d ring=%d smem=%zu",
+           kD, kWarps, kW, kH, kRing, sizeof(JoinSmem));
+  return buf;
+}
+
+int64_t mpgpu_zone_size(int64_t window, double fraction) {
+  if (!(fraction >= 0.0)) return -1;
+  return (int64_t)std::floor((double)window * fraction + 0.5);
+}
+
+int64_t mpgpu_join_cells(int64_t n_a, int64_t n_b, int64_t window, int64_t zone) {
+  const long long La = n_a - window + 1;
+  if (La <= 0) return 0;
+  if (n_b <= 0) {
+    const long long r = La - zone - 1;
+    return r > 0 ? r * (r + 1) / 2 : 0;
+  }
+  const long long Lb = n_b - window + 1;
+  return Lb > 0 ? La * Lb : 0;
+}
+
+mpgpu_status mpgpu_rolling_stats(const double* d_ts, int64_t n, int64_t window, double* d_means,
+                                 double* d_stds, int32_t device, void* cuda_stream) {
+  if (window < 4 || window > n) return fail(MPGPU_EPARAM, "window out of range");
+  MPG_CUDA(cudaSetDevice(device));
+  const long long L = n - window + 1;
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  k_window_stats<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(d_ts, L, (int)window, d_means,
+                                                              nullptr, d_stds, nullptr);
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+mpgpu_plan* mpgpu_plan_create(const double* d_a, int64_t n_a, const double* d_b, int64_t n_b,
+                              int64_t window, int64_t zone, int32_t device, void* cuda_stream) {
+  if (!d_a || window < 4 || window > n_a || (d_b && window > n_b) || zone < 0) {
+    fail(MPGPU_EPARAM, "invalid window / series length / zone");
+    return nullptr;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    fail(MPGPU_ECUDA, "cudaSetDevice failed");
+    return nullptr;
+  }
+  std::unique_ptr<mpgpu_plan> p(new mpgpu_plan());
+  p->device = device;
+  p->self = d_b == nullptr;
+  p->m = window;
+  p->zone = p->self ? zone : 0;
+  if (cuda_stream) {
+    p->stream = (cudaStream_t)cuda_stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      fail(MPGPU_ECUDA, "stream creation failed");
+      return nullptr;
+    }
+    p->own_stream = true;
+  }
+  if (alloc_series(p->A, d_a, n_a, window) != MPGPU_OK) {
+    mpgpu_plan_destroy(p.release());
+    return nullptr;
+  }
+  if (!p->self && alloc_series(p->B, d_b, n_b, window) != MPGPU_OK) {
+    mpgpu_plan_destroy(p.release());
+    return nullptr;
+  }
+  const long long Lb = p->self ? p->A.L : p->B.L;
+  p->index_bits = std::max(1, ceil_log2(std::max(p->A.L, Lb)));
+  if (p->index_bits > 40) {
+    fail(MPGPU_EPARAM, "series too long for packed keys");
+    mpgpu_plan_destroy(p.release());
+    return nullptr;
+  }
+  p->imask = (1LL << p->index_bits) - 1;
+  if (cudaMalloc(&p->key0, sizeof(long long) * p->A.L) != cudaSuccess ||
+      cudaMalloc(&p->key1, sizeof(long long) * Lb) != cudaSuccess ||
+      cudaMalloc(&p->d_counter, sizeof(int)) != cudaSuccess) {
+    fail(MPGPU_ENOMEM, "key allocation failed");
+    mpgpu_plan_destroy(p.release());
+    return nullptr;
+  }
+  build_items(p.get());
+  if (!p->items.empty()) {
+    if (cudaMalloc(&p->d_items, sizeof(Item) * p->items.size()) != cudaSuccess) {
+      fail(MPGPU_ENOMEM, "item allocation failed");
+      mpgpu_plan_destroy(p.release());
+      return nullptr;
+    }
+  }
+  std::call_once(g_attr_once, [] {
+    cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(JoinSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_ctas_per_sm, k_join, kThreads,
+                                                  sizeof(JoinSmem));
+  });
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  // attribute is per-device: set it here as well for multi-device processes
+  cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
+  p->n_ctas = sms * std::max(1, g_ctas_per_sm);
+  return p.release();
+}
+
+void mpgpu_plan_destroy(mpgpu_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  p->A.release();
+  p->B.release();
+  cudaFree(p->key0);
+  cudaFree(p->key1);
+  cudaFree(p->d_items);
+  cudaFree(p->d_counter);
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+}
+
+mpgpu_status mpgpu_plan_prepare(mpgpu_plan* p) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  MPG_CUDA(cudaSetDevice(p->device));
+  p->launches = 0;
+  mpgpu_status st = launch_stats(p, p->A);
+  if (st != MPGPU_OK) return st;
+  if (!p->self && (st = launch_stats(p, p->B)) != MPGPU_OK) return st;
+  const long long L1 = p->self ? p->A.L : p->B.L;
+  k_fill_keys<<<(unsigned)((p->A.L + 255) / 256), 256, 0, p->stream>>>(p->key0, p->A.L);
+  k_fill_keys<<<(unsigned)((L1 + 255) / 256), 256, 0, p->stream>>>(p->key1, L1);
+  p->launches += 2;
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+int64_t mpgpu_plan_shard_cells(const mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  if (!p || n_shards < 1 || shard < 0 || shard >= n_shards) return 0;
+  long long c = 0;
+  for (size_t q = (size_t)shard; q < p->items.size(); q += (size_t)n_shards) c += p->item_cells[q];
+  return c;
+}
+
+mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
+  MPG_CUDA(cudaSetDevice(p->device));
+  std::vector<Item> mine;
+  shard_items(p, shard, n_shards, mine, nullptr);
+  if (mine.empty()) return MPGPU_OK;
+  // each shard uses its own slice of the device item buffer (shards may be
+  // in flight together on one device)
+  size_t off = 0;
+  for (int s = 0; s < shard; ++s) off += (p->items.size() + n_shards - 1 - s) / n_shards;
+  MPG_CUDA(cudaMemcpyAsync(p->d_items + off, mine.data(), sizeof(Item) * mine.size(),
+                           cudaMemcpyHostToDevice, p->stream));
+  MPG_CUDA(cudaMemsetAsync(p->d_counter, 0, sizeof(int), p->stream));
+  JoinParams P = make_params(p);
+  P.items = p->d_items + off;
+  P.n_items = (int)mine.size();
+  P.counter = p->d_counter;
+  const int grid = (int)std::min<long long>((long long)mine.size(), p->n_ctas);
+  k_join<<<grid, kThreads, sizeof(JoinSmem), p->stream>>>(P);
+  p->launches += 1;
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_plan_keys(mpgpu_plan* p, int64_t** d_row_keys, int64_t* row_len,
+                             int64_t** d_col_keys, int64_t* col_len) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (d_row_keys) *d_row_keys = (int64_t*)p->key0;
+  if (row_len) *row_len = p->A.L;
+  if (d_col_keys) *d_col_keys = (int64_t*)p->key1;
+  if (col_len) *col_len = p->self ? p->A.L : p->B.L;
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_plan_finalize(mpgpu_plan* p, double* d_mp_a, int64_t* d_pi_a,
+                                 int64_t* d_left_a, int64_t* d_right_a, double* d_mp_b,
+                                 int64_t* d_pi_b) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  MPG_CUDA(cudaSetDevice(p->device));
+  const int bs = 256;
+  if (p->self) {
+    const long long thr = p->A.L * 32;
+    k_finalize_self<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
+        p->A.view(), p->key0, p->key1, p->zone, (int)p->m, p->imask, d_mp_a,
+        (long long*)d_pi_a, (long long*)d_left_a, (long long*)d_right_a);
+    p->launches += 1;
+  } else {
+    if (d_mp_a || d_pi_a) {
+      const long long thr = p->A.L * 32;
+      k_finalize_ab<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
+          p->A.view(), p->B.view(), p->key0, (int)p->m, p->imask, d_mp_a, (long long*)d_pi_a);
+      p->launches += 1;
+    }
+    if (d_mp_b || d_pi_b) {
+      const long long thr = p->B.L * 32;
+      k_finalize_ab<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
+          p->B.view(), p->A.view(), p->key1, (int)p->m, p->imask, d_mp_b, (long long*)d_pi_b);
+      p->launches += 1;
+    }
+  }
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_keys_min_merge(int64_t* d_dst, const int64_t* d_src, int64_t len,
+                                  int32_t device, void* cuda_stream) {
+  MPG_CUDA(cudaSetDevice(device));
+  if (len <= 0) return MPGPU_OK;
+  k_keys_min<<<(unsigned)((len + 255) / 256), 256, 0, (cudaStream_t)cuda_stream>>>(
+      (long long*)d_dst, (const long long*)d_src, len);
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+int64_t mpgpu_plan_launch_count(const mpgpu_plan* p) { return p ? p->launches : 0; }
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host-buffer join over one or more devices.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&ptr, bytes);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+};
+
+// Per-device cached resources, so repeated joins reuse device memory and
+// plans (the library owns them; SURVEY.md §8b conventions).
+struct DevCtx {
+  std::mutex mu;
+  int device = -1;  // CUDA device
+  int slot = 0;     // >0: extra context on the same device (virtual shards)
+  cudaStream_t stream = nullptr;
+  DevBuf xa, xb, out_mp_a, out_pi_a, out_l, out_r, out_mp_b, out_pi_b, keys_in0, keys_in1;
+  mpgpu_plan* plan = nullptr;
+  long long pa = -1, pb = -1, pm = -1, pz = -1;
+  bool pself = false;
+  const void *pxa = nullptr, *pxb = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<DevCtx>> g_ctx;
+
+DevCtx* get_ctx(int device, int slot) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  for (auto& c : g_ctx)
+    if (c->device == device && c->slot == slot) return c.get();
+  g_ctx.emplace_back(new DevCtx());
+  DevCtx* c = g_ctx.back().get();
+  c->device = device;
+  c->slot = slot;
+  return c;
+}
+
+mpgpu_status ensure_ctx(DevCtx* c) {
+  MPG_CUDA(cudaSetDevice(c->device));
+  if (!c->stream) MPG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  if (!c->e0) MPG_CUDA(cudaEventCreate(&c->e0));
+  if (!c->e1) MPG_CUDA(cudaEventCreate(&c->e1));
+  return MPGPU_OK;
+}
+
+mpgpu_status ctx_plan(DevCtx* c, const mpgpu_join_args* a) {
+  const bool self = a->b == nullptr;
+  const long long nb = self ? 0 : a->n_b;
+  if (c->plan && c->pa == a->n_a && c->pb == nb && c->pm == a->window &&
+      c->pz == (self ? a->zone : 0) && c->pself == self && c->pxa == c->xa.ptr &&
+      c->pxb == (self ? nullptr : c->xb.ptr))
+    return MPGPU_OK;
+  if (c->plan) {
+    mpgpu_plan_destroy(c->plan);
+    c->plan = nullptr;
+  }
+  c->plan = mpgpu_plan_create((const double*)c->xa.ptr, a->n_a,
+                              self ? nullptr : (const double*)c->xb.ptr, nb, a->window,
+                              self ? a->zone : 0, c->device, c->stream);
+  if (!c->plan) return MPGPU_ECUDA;
+  c->pa = a->n_a;
+  c->pb = nb;
+  c->pm = a->window;
+  c->pz = self ? a->zone : 0;
+  c->pself = self;
+  c->pxa = c->xa.ptr;
+  c->pxb = self ? nullptr : c->xb.ptr;
+  return MPGPU_OK;
+}
+
+mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* total_ms) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (!a || !a->a) return fail(MPGPU_EPARAM, "null arguments");
+  const bool self = a->b == nullptr;
+  if (a->window < 4) return fail(MPGPU_EPARAM, "window below minimum 4");
+  if (a->window > a->n_a || (!self && a->window > a->n_b))
+    return fail(MPGPU_EPARAM, "series shorter than the window");
+  if (a->zone < 0) return fail(MPGPU_EPARAM, "negative exclusion zone");
+  const int ng = a->n_gpus > 0 ? a->n_gpus : 1;
+  std::vector<int> devs(ng);
+  for (int g = 0; g < ng; ++g) devs[g] = a->devices ? a->devices[g] : g;
+  const long long La = a->n_a - a->window + 1;
+  const long long Lb = self ? La : a->n_b - a->window + 1;
+
+  std::vector<DevCtx*> ctx(ng);
+  // distinct contexts even when a device id repeats (virtual shards on one GPU)
+  for (int g = 0; g < ng; ++g) {
+    int dup = 0;
+    for (int h = 0; h < g; ++h) dup += devs[h] == devs[g];
+    ctx[g] = get_ctx(devs[g], dup);
+  }
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int g = 0; g < ng; ++g) locks.emplace_back(ctx[g]->mu);
+  auto real = [](const DevCtx* c) { return c->device; };
+
+  // 1) device buffers + cached plan on every device
+  for (int g = 0; g < ng; ++g) {
+    DevCtx* c = ctx[g];
+    mpgpu_status st = ensure_ctx(c);
+    if (st != MPGPU_OK) return st;
+    MPG_CUDA(c->xa.ensure(sizeof(double) * a->n_a));
+    if (!self) MPG_CUDA(c->xb.ensure(sizeof(double) * a->n_b));
+    st = ctx_plan(c, a);
+    if (st != MPGPU_OK) return st;
+  }
+  for (int g = 0; g < ng; ++g) {
+    DevCtx* c = ctx[g];
+    MPG_CUDA(cudaSetDevice(real(c)));
+    MPG_CUDA(cudaEventRecord(c->e0, c->stream));
+    MPG_CUDA(cudaMemcpyAsync(c->xa.ptr, a->a, sizeof(double) * a->n_a, cudaMemcpyHostToDevice,
+                             c->stream));
+    if (!self)
+      MPG_CUDA(cudaMemcpyAsync(c->xb.ptr, a->b, sizeof(double) * a->n_b, cudaMemcpyHostToDevice,
+                               c->stream));
+    mpgpu_status st = mpgpu_plan_prepare(c->plan);
+    if (st != MPGPU_OK) return st;
+    if (!a->progress) {
+      st = mpgpu_plan_run(c->plan, g, ng);
+      if (st != MPGPU_OK) return st;
+    }
+  }
+  if (a->progress) {
+    // run each device's shard in sub-shards and report after each completes
+    const int sub = 16;
+    for (int q = 0; q < sub; ++q) {
+      for (int g = 0; g < ng; ++g) {
+        mpgpu_status st = mpgpu_plan_run(ctx[g]->plan, g * sub + q, ng * sub);
+        if (st != MPGPU_OK) return st;
+      }
+      for (int g = 0; g < ng; ++g) {
+        MPG_CUDA(cudaSetDevice(real(ctx[g])));
+        MPG_CUDA(cudaStreamSynchronize(ctx[g]->stream));
+      }
+      a->progress((double)(q + 1) / sub, a->progress_ctx);
+    }
+  }
+  // 2) min-merge shard keys into device 0 (peer copies over NVLink)
+  DevCtx* c0 = ctx[0];
+  if (ng > 1) {
+    int64_t *k0r, *k0c;
+    mpgpu_plan_keys(c0->plan, &k0r, nullptr, &k0c, nullptr);
+    MPG_CUDA(cudaSetDevice(real(c0)));
+    MPG_CUDA(c0->keys_in0.ensure(sizeof(long long) * La));
+    MPG_CUDA(c0->keys_in1.ensure(sizeof(long long) * Lb));
+    for (int g = 1; g < ng; ++g) {
+      DevCtx* c = ctx[g];
+      int64_t *kr, *kc;
+      mpgpu_plan_keys(c->plan, &kr, nullptr, &kc, nullptr);
+      cudaEvent_t done;
+      MPG_CUDA(cudaSetDevice(real(c)));
+      MPG_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+      MPG_CUDA(cudaEventRecord(done, c->stream));
+      MPG_CUDA(cudaSetDevice(real(c0)));
+      MPG_CUDA(cudaStreamWaitEvent(c0->stream, done, 0));
+      if (real(c) != real(c0)) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, real(c0), real(c));
+        if (can) {
+          cudaError_t pe = cudaDeviceEnablePeerAccess(real(c), 0);
+          if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        }
+        MPG_CUDA(cudaMemcpyPeerAsync(c0->keys_in0.ptr, real(c0), kr, real(c),
+                                     sizeof(long long) * La, c0->stream));
+        MPG_CUDA(cudaMemcpyPeerAsync(c0->keys_in1.ptr, real(c0), kc, real(c),
+                                     sizeof(long long) * Lb, c0->stream));
+      } else {
+        MPG_CUDA(cudaMemcpyAsync(c0->keys_in0.ptr, kr, sizeof(long long) * La,
+                                 cudaMemcpyDeviceToDevice, c0->stream));
+        MPG_CUDA(cudaMemcpyAsync(c0->keys_in1.ptr, kc, sizeof(long long) * Lb,
+                                 cudaMemcpyDeviceToDevice, c0->stream));
+      }
+      mpgpu_status st = mpgpu_keys_min_merge(k0r, (const int64_t*)c0->keys_in0.ptr, La, real(c0),
+                                             c0->stream);
+      if (st != MPGPU_OK) return st;
+      st = mpgpu_keys_min_merge(k0c, (const int64_t*)c0->keys_in1.ptr, Lb, real(c0), c0->stream);
+      if (st != MPGPU_OK) return st;
+      cudaEventDestroy(done);
+    }
+  }
+  // 3) finalize on device 0 and copy back
+  MPG_CUDA(cudaSetDevice(real(c0)));
+  MPG_CUDA(c0->out_mp_a.ensure(sizeof(double) * La));
+  MPG_CUDA(c0->out_pi_a.ensure(sizeof(long long) * La));
+  if (self) {
+    MPG_CUDA(c0->out_l.ensure(sizeof(long long) * La));
+    MPG_CUDA(c0->out_r.ensure(sizeof(long long) * La));
+  } else {
+    MPG_CUDA(c0->out_mp_b.ensure(sizeof(double) * Lb));
+    MPG_CUDA(c0->out_pi_b.ensure(sizeof(long long) * Lb));
+  }
+  mpgpu_status st = mpgpu_plan_finalize(
+      c0->plan, (double*)c0->out_mp_a.ptr, (int64_t*)c0->out_pi_a.ptr,
+      self ? (int64_t*)c0->out_l.ptr : nullptr, self ? (int64_t*)c0->out_r.ptr : nullptr,
+      (!self && (a->mp_b || a->pi_b)) ? (double*)c0->out_mp_b.ptr : nullptr,
+      (!self && (a->mp_b || a->pi_b)) ? (int64_t*)c0->out_pi_b.ptr : nullptr);
+  if (st != MPGPU_OK) return st;
+  MPG_CUDA(cudaEventRecord(c0->e1, c0->stream));
+  auto d2h = [&](void* dst, const DevBuf& src, size_t bytes) -> cudaError_t {
+    if (!dst) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src.ptr, bytes, cudaMemcpyDeviceToHost, c0->stream);
+  };
+  MPG_CUDA(d2h(a->mp_a, c0->out_mp_a, sizeof(double) * La));
+  MPG_CUDA(d2h(a->pi_a, c0->out_pi_a, sizeof(long long) * La));
+  if (self) {
+    MPG_CUDA(d2h(a->left_a, c0->out_l, sizeof(long long) * La));
+    MPG_CUDA(d2h(a->right_a, c0->out_r, sizeof(long long) * La));
+  } else {
+    MPG_CUDA(d2h(a->mp_b, c0->out_mp_b, sizeof(double) * Lb));
+    MPG_CUDA(d2h(a->pi_b, c0->out_pi_b, sizeof(long long) * Lb));
+  }
+  MPG_CUDA(cudaStreamSynchronize(c0->stream));
+  if (kernel_ms) {
+    float ms = 0.f;
+    MPG_CUDA(cudaEventElapsedTime(&ms, c0->e0, c0->e1));
+    *kernel_ms = ms;
+  }
+  if (total_ms)
+    *total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                    .count();
+  return MPGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+mpgpu_status mpgpu_join(const mpgpu_join_args* args) { return join_impl(args, nullptr, nullptr); }
+
+mpgpu_status mpgpu_join_timed(const mpgpu_join_args* args, double* kernel_ms, double* total_ms) {
+  return join_impl(args, kernel_ms, total_ms);
+}
+
+}  // extern "C"

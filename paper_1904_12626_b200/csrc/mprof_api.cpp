@@ -1,0 +1,148 @@
+// C++ shim: the reference's mprof::stomp / mprof::scrimp signatures
+// (profile.hpp:80-89) on top of the C ABI (include/mprof_gpu.h). Status codes
+// come back as the reference's exception types (error.hpp:9-19).
+#include <cmath>
+#include <string>
+#include <utility>
+
+#include "mprof/profile.hpp"
+#include "mprof_gpu.h"
+
+namespace mprof {
+
+TimeSeries::TimeSeries(std::vector<double> values) : data_(std::move(values)) {
+  if (size() < kMinWindow)
+    throw ParameterError("time series too short: length " + std::to_string(size()) +
+                         " < minimum " + std::to_string(kMinWindow));
+  for (std::size_t i = 0; i < data_.size(); ++i)
+    if (!std::isfinite(data_[i]))
+      throw ParameterError("time series sample " + std::to_string(i) + " is not finite");
+}
+
+const char *mode_name(Mode mode) {
+  switch (mode) {
+    case Mode::brute: return "brute";
+    case Mode::stamp: return "stamp";
+    case Mode::stomp: return "stomp";
+    case Mode::scrimp: return "scrimp";
+    case Mode::mstomp: return "mstomp";
+    case Mode::simple: return "simple";
+  }
+  return "?";
+}
+
+std::optional<Mode> mode_from_name(const std::string &name) {
+  for (Mode m : {Mode::brute, Mode::stamp, Mode::stomp, Mode::scrimp, Mode::mstomp, Mode::simple})
+    if (name == mode_name(m)) return m;
+  return std::nullopt;
+}
+
+Index zone_size(Index window, double fraction) {
+  if (!(fraction >= 0.0)) throw ParameterError("exclusion-zone fraction must be >= 0");
+  return static_cast<Index>(mpgpu_zone_size(window, fraction));
+}
+
+namespace {
+
+void check_window(Index window, Index n, const char *which) {
+  if (window < kMinWindow)
+    throw ParameterError("window " + std::to_string(window) + " < minimum " +
+                         std::to_string(kMinWindow));
+  if (window > n)
+    throw ParameterError(std::string("window ") + std::to_string(window) + " exceeds " + which +
+                         " length " + std::to_string(n));
+}
+
+[[noreturn]] void raise(mpgpu_status st) {
+  const std::string msg = mpgpu_last_error();
+  if (st == MPGPU_EUNSUPPORTED) throw UnsupportedError(msg);
+  if (st == MPGPU_EPARAM) throw ParameterError(msg);
+  throw std::runtime_error("mprof_b200: " + msg);
+}
+
+void progress_tramp(double f, void *ctx) { (*static_cast<const ProgressFn *>(ctx))(f); }
+
+MatrixProfile run_join(const TimeSeries &a, const TimeSeries *b, Index window, Index zone,
+                       const ProgressFn &progress, bool want_b_side) {
+  const Index La = a.size() - window + 1;
+  MatrixProfile mp;
+  mp.window = window;
+  mp.exclusion_zone = b ? 0 : zone;
+  mp.join_kind = b ? JoinKind::ab : JoinKind::self;
+  mp.data_len = a.size();
+  mp.data_len_b = b ? b->size() : 0;
+  mpgpu_join_args args{};
+  args.a = a.values().data();
+  args.n_a = a.size();
+  args.b = b ? b->values().data() : nullptr;
+  args.n_b = b ? b->size() : 0;
+  args.window = window;
+  args.zone = mp.exclusion_zone;
+  args.n_gpus = 1;
+  if (want_b_side) {
+    const Index Lb = b->size() - window + 1;
+    mp.values.resize(Lb);
+    mp.index.resize(Lb);
+    args.mp_b = mp.values.data();
+    args.pi_b = mp.index.data();
+  } else {
+    mp.values.resize(La);
+    mp.index.resize(La);
+    args.mp_a = mp.values.data();
+    args.pi_a = mp.index.data();
+    if (!b) {
+      mp.left_index.resize(La);
+      mp.right_index.resize(La);
+      args.left_a = mp.left_index.data();
+      args.right_a = mp.right_index.data();
+    }
+  }
+  if (progress) {
+    args.progress = progress_tramp;
+    args.progress_ctx = const_cast<ProgressFn *>(&progress);
+  }
+  const mpgpu_status st = mpgpu_join(&args);
+  if (st != MPGPU_OK) raise(st);
+  return mp;
+}
+
+}  // namespace
+
+MatrixProfile stomp(const TimeSeries &ts_a, const TimeSeries *ts_b, Index window,
+                    double ez_fraction, int n_workers, const ProgressFn &progress) {
+  if (n_workers < 1) throw ParameterError("n_workers must be >= 1");
+  check_window(window, ts_a.size(), "series");
+  if (ts_b) check_window(window, ts_b->size(), "series B");
+  const Index zone = zone_size(window, ez_fraction);
+  MatrixProfile mp = run_join(ts_a, ts_b, window, zone, progress, false);
+  mp.mode = Mode::stomp;
+  return mp;
+}
+
+MatrixProfile scrimp(const TimeSeries &ts_a, Index window, double ez_fraction, Index s_size,
+                     std::uint64_t seed, const ProgressFn &progress) {
+  if (s_size < 1) throw ParameterError("s_size must be >= 1");
+  check_window(window, ts_a.size(), "series");
+  const Index zone = zone_size(window, ez_fraction);
+  const Index L = ts_a.size() - window + 1;
+  const Index n_diag = L > zone + 1 ? L - zone - 1 : 0;
+  if (s_size < n_diag)
+    throw UnsupportedError("anytime SCRIMP (s_size < number of diagonals) is not provided by "
+                           "the B200 backend; pass kFullRun");
+  MatrixProfile mp = run_join(ts_a, nullptr, window, zone, progress, false);
+  mp.mode = Mode::scrimp;
+  mp.seed = seed;
+  return mp;
+}
+
+MatrixProfile stomp_ab_reverse(const TimeSeries &ts_a, const TimeSeries &ts_b, Index window) {
+  check_window(window, ts_a.size(), "series");
+  check_window(window, ts_b.size(), "series B");
+  MatrixProfile mp = run_join(ts_a, &ts_b, window, 0, {}, true);
+  mp.mode = Mode::stomp;
+  mp.data_len = ts_b.size();
+  mp.data_len_b = ts_a.size();
+  return mp;
+}
+
+}  // namespace mprof
