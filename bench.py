@@ -1,0 +1,355 @@
+#!/usr/bin/env python3
+"""Benchmark: matrix-profile cells/s of the B200 join (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+Step = one full self-join of the workload (window stats + diagonal tiles +
+finalize) with inputs resident in HBM. N=1 runs C4 (n=2^20, m=256, ECG-like,
+the headline metric's shape). Under torchrun (N>1) every rank evaluates an
+equal-cell shard of the diagonal work items, the packed int64 keys are
+min-reduced over NCCL (torch.distributed, ReduceOp.MIN) and rank 0 finalizes
+(strong scaling: total work fixed). Rank 0 prints ONE JSON line.
+
+`--impl reference` times the CPU restatement of the reference STOMP
+(oracle/, the reference itself cannot be compiled: SURVEY.md §0) on the host
+cores over a bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Measured on this pool's B200 (profiles/fp64_peak_r01.jsonl, tools/microbench):
+# DMUL 1.858e13/s, DFMA 1.711e13/s at 1965 MHz -> 148 SMs x 64 fp64 lanes x clock.
+FP64_OPS_PER_CLK_SM = 64
+N_SM = 148
+FP64_PEAK_MEASURED = 1.858e13  # fp64 pipe ops/s, burst, 1965 MHz
+FP64_OPS_PER_CELL = 4          # 2 DFMA (cov recurrence) + 2 DMUL (normalise); compares on ALU
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        mhz, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                mhz.append(float(r[0]))
+                mx = float(r[1])
+                for n, v in zip(names, r[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(mhz)}
+
+
+def cpu_sample_rate(cfg, seconds_target=15.0, threads=None):
+    """Oracle STOMP (restated reference, oracle/) on a bounded row sample.
+
+    Returns (unique-cells/s, threads, sample description). Full STOMP rows cost
+    L evaluations each and L rows cover the (L-z-1)(L-z)/2 unique cells, so a
+    sample of R rows stands for R/L of the job."""
+    import oracle
+    threads = threads or oracle.default_threads()
+    L = cfg.a.size - cfg.window + 1
+    rows = 4096
+    t0 = time.perf_counter()
+    oracle.stomp(cfg.a, cfg.b, cfg.window, cfg.ez, n_workers=threads, row_begin=0, row_end=rows)
+    dt = time.perf_counter() - t0
+    if dt < seconds_target / 3:
+        rows = int(min(L, max(rows, rows * seconds_target / max(dt, 1e-3))))
+        rows = max(4096, (rows // 4096) * 4096)
+        t0 = time.perf_counter()
+        oracle.stomp(cfg.a, cfg.b, cfg.window, cfg.ez, n_workers=threads, row_begin=0, row_end=rows)
+        dt = time.perf_counter() - t0
+    Lrows = (cfg.b.size - cfg.window + 1) if cfg.b is not None else L
+    rate = cfg.cells() * (rows / Lrows) / dt
+    return rate, threads, f"oracle STOMP rows [0,{rows}) of {Lrows} ({dt:.1f}s, full rows), extrapolated to unique cells"
+
+
+def flush_l2(buf):
+    buf.add_(1)
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU restatement of the reference STOMP."""
+    if rank != 0:
+        return
+    samples = []
+    threads = None
+    desc = ""
+    for s in range(args.warmup + args.steps):
+        rate, threads, desc = cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
+        if s >= args.warmup:
+            samples.append(rate)
+    v = statistics.median(samples)
+    line = {
+        "impl": "reference", "metric": "matrix-profile cells/sec", "value": v, "unit": "cells/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": cfg.cells() / v * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, datasets.py)",
+        "config": {"workload": cfg.description, "config": cfg.name, "cells_per_step": cfg.cells()},
+        "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+
+    from paper_1904_12626_b200 import datasets
+    cfg = datasets.get(args.config)
+
+    if args.impl == "reference":
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")
+        run_reference(args, cfg, rank, world)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    import torch
+    import paper_1904_12626_b200 as mp
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    stream = torch.cuda.Stream(dev)
+    a = torch.from_numpy(cfg.a).to(dev)
+    b = torch.from_numpy(cfg.b).to(dev) if cfg.b is not None else None
+    with torch.cuda.stream(stream):
+        plan = mp.Plan(a, b, cfg.window, cfg.zone, stream=stream)
+    cells_total = plan.cells(0, 1)
+    assert cells_total == cfg.cells(), (cells_total, cfg.cells())
+    my_cells = plan.cells(rank, world)
+    l2 = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    outs = None
+
+    def step(ev):
+        nonlocal outs
+        ev[0].record(stream)
+        plan.prepare()
+        ev[1].record(stream)
+        plan.run(rank, world)
+        ev[2].record(stream)
+        if world > 1:
+            rk, ck = plan.keys()
+            with torch.cuda.stream(stream):
+                dist.all_reduce(rk, op=dist.ReduceOp.MIN)
+                dist.all_reduce(ck, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            with torch.cuda.stream(stream):
+                outs = plan.outputs()
+        ev[3].record(stream)
+
+    mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            flush_l2(l2)
+        step(mk())
+    torch.cuda.synchronize()
+    launches_per_step = plan.launches() + (0 if rank else 0)
+
+    evs = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush_l2(l2)
+            e = mk()
+            step(e)
+            evs.append(e)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    join_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    total_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([total_ms, statistics.mean(join_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, join_avg = float(t[0]), float(t[1])
+    else:
+        join_avg = statistics.mean(join_ms)
+    ms_per_step = total_ms / args.steps
+    value = cells_total / (ms_per_step * 1e-3)
+
+    # roofline of the dominant kernel (k_join): algorithmic fp64 pipe ops / launch time
+    join_ops_per_s = my_cells * FP64_OPS_PER_CELL / (join_avg * 1e-3)
+    csum = clk.summary()
+
+    # e2e through the public host API: pinned host series -> H2D -> join -> D2H
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_measure(args, cfg, mp, rank, world, dev, dist)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, thr, desc = cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
+        cpu = {"value": rate, "unit": "cells/s", "cores": thr, "kind": "port", "sample": desc}
+
+    if rank == 0:
+        prof = os.path.join(ROOT, "profiles", "k_join_traffic.json")
+        traffic = None
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("dram_bytes_per_launch")
+            except (OSError, ValueError):
+                traffic = None
+        line = {
+            "metric": "matrix-profile cells/sec", "value": value, "unit": "cells/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, datasets.py)",
+            "config": {"workload": cfg.description, "config": cfg.name, "cells_per_step": cells_total,
+                       "window": cfg.window, "exclusion_zone": cfg.zone,
+                       "l2": "flushed between steps (256 MB write)",
+                       "parallelism": f"diagonal shards x{world}, NCCL MIN merge" if world > 1 else "1 GPU",
+                       "tile": mp.lib().mpgpu_build_info().decode()},
+            "roofline": {"bound": "fp64", "kernel": "k_join",
+                         "achieved": join_ops_per_s / 1e12, "peak": FP64_PEAK_MEASURED / 1e12,
+                         "unit": "Tops/s (fp64 pipe: DFMA+DMUL, 4 per cell)",
+                         "frac": join_ops_per_s / FP64_PEAK_MEASURED,
+                         "traffic": traffic, "join_ms_per_launch": join_avg,
+                         "cells_per_launch": my_cells,
+                         "peak_source": "measured fp64 microbench (profiles/fp64_peak_r01.jsonl), burst 1965 MHz"},
+            "clocks": csum,
+            "gpu_launches": launches_per_step * args.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_measure(args, cfg, mp, rank, world, dev, dist):
+    """Same metric through the host-facing API with host buffers.
+
+    1 GPU: mpgpu_join (C ABI) from pinned host memory, outputs copied back.
+    N GPUs: each rank copies the pinned series in, runs its shard, keys are
+    MIN-reduced over NCCL, rank 0 finalizes and copies the profile out."""
+    import torch
+    L = cfg.a.size - cfg.window + 1
+    pinned_a = torch.from_numpy(cfg.a).pin_memory()
+    pinned_b = torch.from_numpy(cfg.b).pin_memory() if cfg.b is not None else None
+    h2d = cfg.a.nbytes + (cfg.b.nbytes if cfg.b is not None else 0)
+    d2h = L * 8 * (4 if cfg.b is None else 2)
+    times = []
+    if world == 1:
+        A = pinned_a.numpy()
+        B = pinned_b.numpy() if pinned_b is not None else None
+        for s in range(args.warmup + args.steps):
+            r = mp.join(A, B, cfg.window, cfg.zone, want_b=False, timed=True)
+            if s >= args.warmup:
+                times.append(r["total_ms"])
+        t = sum(times) / len(times)
+    else:
+        stream = torch.cuda.Stream(dev)
+        out_host = {}
+        for s in range(args.warmup + args.steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            with torch.cuda.stream(stream):
+                a = pinned_a.to(dev, non_blocking=True)
+                b = pinned_b.to(dev, non_blocking=True) if pinned_b is not None else None
+                plan = mp.Plan(a, b, cfg.window, cfg.zone, stream=stream)
+                plan.prepare()
+                plan.run(rank, world)
+                rk, ck = plan.keys()
+                dist.all_reduce(rk, op=dist.ReduceOp.MIN)
+                dist.all_reduce(ck, op=dist.ReduceOp.MIN)
+                if rank == 0:
+                    o = plan.outputs()
+                    for k, v in o.items():
+                        out_host[k] = v.to("cpu", non_blocking=True)
+            stream.synchronize()
+            dt = (time.perf_counter() - t0) * 1e3
+            plan.close()
+            tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            if s >= args.warmup:
+                times.append(float(tt[0]))
+        t = sum(times) / len(times)
+    return {"value": cfg.cells() / (t * 1e-3), "unit": "cells/s", "ms_per_step": t,
+            "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h,
+            "api": "mpgpu_join (C ABI)" if world == 1 else "Plan + torch.distributed NCCL MIN"}
+
+
+if __name__ == "__main__":
+    main()
