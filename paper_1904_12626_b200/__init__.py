@@ -31,7 +31,7 @@ K_FULL_RUN = (1 << 63) - 1   # kFullRun (profile.hpp:20-21)
 MIN_WINDOW = 4               # kMinWindow (types.hpp:19-21)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libmprof_b200.so")
+_LIB_PATH = os.environ.get("MPGPU_LIB") or os.path.join(_HERE, "libmprof_b200.so")
 _lib = None
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -348,9 +348,13 @@ class Plan:
         self._p = ctypes.c_void_p(p)
 
     def close(self) -> None:
-        if getattr(self, "_p", None):
-            lib().mpgpu_plan_destroy(self._p)
-            self._p = None
+        p = getattr(self, "_p", None)
+        if p and _lib is not None:
+            try:
+                _lib.mpgpu_plan_destroy(p)
+            except Exception:  # interpreter shutdown
+                pass
+        self._p = None
 
     __del__ = close
 

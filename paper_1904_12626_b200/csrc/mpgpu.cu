@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -157,8 +158,9 @@ void build_items(mpgpu_plan* p) {
     // sum_k min(LR, LC - k) over k in [klo, khi)
     cells += sum_clamp(g.LC, g.klo, g.khi, g.LR);
   }
-  const long long ref_ctas = 296;  // 148 SMs x 2 CTAs (fixed: independent of device & shards)
-  long long seg = cells / ((long long)kW * 64 * ref_ctas);
+  // 148 SMs x kMinBlocks CTAs x kWarps warp-workers (fixed: independent of device & shards)
+  const long long ref_workers = 148LL * kMinBlocks * kWarps;
+  long long seg = cells / ((long long)kW * 64 * ref_workers);
   seg = std::max<long long>(kH, std::min<long long>(16384, seg));
   seg = (seg / kH) * kH;
   p->seg_rows = seg;
@@ -380,6 +382,18 @@ mpgpu_status mpgpu_plan_prepare(mpgpu_plan* p) {
   k_fill_keys<<<(unsigned)((p->A.L + 255) / 256), 256, 0, p->stream>>>(p->key0, p->A.L);
   k_fill_keys<<<(unsigned)((L1 + 255) / 256), 256, 0, p->stream>>>(p->key1, L1);
   p->launches += 2;
+  // warm-start keys on a few spread diagonals of every pass
+  JoinParams P = make_params(p);
+  const int npass = p->self ? 1 : 2;
+  for (int q = 0; q < npass; ++q) {
+    const Pass& ps = P.pass[q];
+    const long long klo = p->self ? p->zone + 1 : (q == 0 ? 0 : 1);
+    const long long khi = ps.C.L;
+    if (khi <= klo) continue;
+    dim3 grid((unsigned)((ps.R.L + 255) / 256), kInitDiag);
+    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask);
+    p->launches += 1;
+  }
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
 }
@@ -409,10 +423,28 @@ mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
   P.items = p->d_items + off;
   P.n_items = (int)mine.size();
   P.counter = p->d_counter;
-  const int grid = (int)std::min<long long>((long long)mine.size(), p->n_ctas);
+  const int grid = (int)std::min<long long>(((long long)mine.size() + kWarps - 1) / kWarps, p->n_ctas);
+  static const bool want_stats = getenv("MPGPU_STATS") && atoi(getenv("MPGPU_STATS")) > 0;
+  unsigned long long* d_stats = nullptr;
+  if (want_stats) {
+    MPG_CUDA(cudaMalloc(&d_stats, 8 * sizeof(unsigned long long)));
+    MPG_CUDA(cudaMemsetAsync(d_stats, 0, 8 * sizeof(unsigned long long), p->stream));
+    P.stats = d_stats;
+  }
   k_join<<<grid, kThreads, sizeof(JoinSmem), p->stream>>>(P);
   p->launches += 1;
   MPG_CUDA(cudaGetLastError());
+  if (want_stats) {
+    unsigned long long h[8];
+    MPG_CUDA(cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
+    MPG_CUDA(cudaStreamSynchronize(p->stream));
+    long long cells = 0;
+    for (auto& it : mine) { (void)it; }
+    for (size_t q = (size_t)shard; q < p->items.size(); q += (size_t)n_shards) cells += p->item_cells[q];
+    fprintf(stderr, "[mpgpu stats] cells %lld warp_row_steps %.3e slow_entries %llu (%.4f%%) row_cand %llu col_cand %llu\n",
+            cells, cells / 256.0, h[0], 100.0 * h[0] / (cells / 256.0), h[1], h[2]);
+    cudaFree(d_stats);
+  }
   return MPGPU_OK;
 }
 
