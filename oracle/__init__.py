@@ -55,6 +55,8 @@ def _load():
                                  ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _dp, _ip, _ip, _ip]
         lib.or_scrimp.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
                                   ctypes.c_uint64, _dp, _ip, _ip, _ip, _dp]
+        lib.or_apply_exclusion_zone.restype = None
+        lib.or_apply_exclusion_zone.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
         lib.or_merge_min.restype = None
         lib.or_merge_min.argtypes = [_dp, _ip, _dp, ctypes.c_int64, ctypes.c_int64]
         _lib = lib
@@ -170,6 +172,12 @@ def scrimp(a, w=4, ez=0.5, s_size=0, seed=0):
     if rc:
         raise ValueError("invalid window / fraction")
     return mp, pi, le, ri, cov.value
+
+
+def apply_exclusion_zone(dp, center, zone):
+    dp = _f64(dp).copy()
+    _load().or_apply_exclusion_zone(_d(dp), dp.size, int(center), int(zone))
+    return dp
 
 
 def merge_min(acc, acc_idx, dp, source_index):

@@ -81,6 +81,13 @@ int or_sliding_dot_direct(const double *q, int64_t w, const double *ts, int64_t 
   return 0;
 }
 
+/* apply_exclusion_zone_inplace (distance.hpp:22-24):
+ * |i - center| <= zone -> +inf. */
+void or_apply_exclusion_zone(double *dp, int64_t len, int64_t center, int64_t zone) {
+  const int64_t lo = imax64(0, center - zone), hi = imin64(len - 1, center + zone);
+  for (int64_t i = lo; i <= hi; ++i) dp[i] = INFINITY;
+}
+
 /* merge_min (profile.hpp:66-68). */
 void or_merge_min(double *acc, int64_t *acc_idx, const double *dp, int64_t len,
                   int64_t source_index) {
@@ -349,6 +356,12 @@ int or_stomp(const double *a, int64_t n_a, const double *b, int64_t n_b, int64_t
     }
     mp[j] = sqrt(v);
     pi[j] = p;
+    /* Near-zero hits are recomputed directly so exact matches come out as 0
+     * (the reference's convention for distance profiles, distance.hpp:30-33);
+     * the QT formula cancels to ~sqrt(2w*eps) there. */
+    if (p >= 0 && mp[j] < 1e-3) {
+      mp[j] = direct_dist(a + j, ma[j] + ga, sa[j], b + p, mb[p] + (self ? ga : gb), sb[p], w);
+    }
     if (left) left[j] = self ? li : -1;
     if (right) right[j] = self ? ri : -1;
   }

@@ -1,0 +1,40 @@
+"""Multi-GPU join: one process per GPU, diagonal shards, NCCL MIN merge.
+
+Every rank holds the whole series, evaluates an equal-cell shard of the
+diagonal work items (mpgpu_plan_run(shard=rank, n_shards=world)), and the
+packed int64 keys are min-reduced across ranks — the only exchange the join
+has. Rank `root` then decodes the keys into the profile.
+Shards never change the arithmetic of a cell, so the result is bit-identical
+for any world size.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+
+def merge_keys_(row_keys, col_keys, group=None, root: Optional[int] = None) -> None:
+    """In-place elementwise MIN of both key arrays across the group.
+
+    root=None: all-reduce (every rank gets the merged keys); otherwise reduce
+    to `root` only."""
+    import torch.distributed as dist
+    op = dist.ReduceOp.MIN
+    for t in (row_keys, col_keys):
+        if root is None:
+            dist.all_reduce(t, op=op, group=group)
+        else:
+            dist.reduce(t, dst=root, op=op, group=group)
+
+
+def sharded_join(plan, rank: int, world: int, group=None, root: int = 0):
+    """Run one rank's shard of `plan` (a paper_1904_12626_b200.Plan) and merge.
+
+    Returns the MatrixProfile device arrays on `root`, None elsewhere."""
+    plan.prepare()
+    plan.run(rank, world)
+    if world > 1:
+        rk, ck = plan.keys()
+        merge_keys_(rk, ck, group=group, root=root)
+    if rank == root:
+        return plan.outputs()
+    return None

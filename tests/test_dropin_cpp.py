@@ -1,0 +1,81 @@
+"""The reference's C++ API as a drop-in: a caller compiled against
+include/mprof/profile.hpp and linked to libmprof_b200.so (GPU)."""
+import json
+import os
+import shutil
+import subprocess
+
+import numpy as np
+import pytest
+
+from tests.parity import close, index_mismatches
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def exe(tmp_path_factory):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    gxx = shutil.which("g++")
+    libdir = os.path.join(ROOT, "paper_1904_12626_b200")
+    out = str(tmp_path_factory.mktemp("cpp") / "dropin_example")
+    r = subprocess.run([gxx, "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "dropin_example.cpp"), "-L" + libdir,
+                        "-lmprof_b200", "-Wl,-rpath," + libdir, "-o", out],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+def _run(exe, tmp_path, a, w, ez, mode="stomp", b=None):
+    inp = tmp_path / "a.f64"
+    a.astype(np.float64).tofile(inp)
+    args = [exe, str(inp), str(w), str(ez), str(tmp_path / "out"), mode]
+    if b is not None:
+        bp = tmp_path / "b.f64"
+        b.astype(np.float64).tofile(bp)
+        args.append(str(bp))
+    r = subprocess.run(args, capture_output=True, text=True)
+    info = json.loads(r.stdout.strip().splitlines()[-1])
+    res = {k: np.fromfile(tmp_path / f"out.{k}", dtype=np.float64 if k == "mp" else np.int64)
+           for k in ("mp", "pi", "left", "right")} if r.returncode == 0 else None
+    return r.returncode, info, res
+
+
+def test_cpp_stomp_self_join(exe, tmp_path, oracle_lib):
+    x = np.cumsum(np.random.default_rng(8).standard_normal(3000))
+    rc, info, res = _run(exe, tmp_path, x, 64, 0.5)
+    assert rc == 0 and info["size"] == x.size - 63 and info["zone"] == 32
+    assert info["mode"] == "stomp" and info["progress_calls"] >= 1
+    ref = oracle_lib.stomp(x, None, 64, 0.5, n_workers=4)
+    assert close(res["mp"], ref[0])[0]
+    rows = np.arange(res["mp"].size)
+    assert not index_mismatches(res["pi"], ref[1], rows, x, x, 64)
+    assert not index_mismatches(res["left"], ref[2], rows, x, x, 64)
+    assert not index_mismatches(res["right"], ref[3], rows, x, x, 64)
+
+
+def test_cpp_scrimp_and_ab(exe, tmp_path, oracle_lib):
+    g = np.random.default_rng(9)
+    x = np.cumsum(g.standard_normal(2000))
+    rc, info, res = _run(exe, tmp_path, x, 50, 0.25, "scrimp")
+    assert rc == 0 and info["mode"] == "scrimp"
+    ref = oracle_lib.stomp(x, None, 50, 0.25)
+    assert close(res["mp"], ref[0])[0]
+    y = np.cumsum(g.standard_normal(900))
+    rc, info, res = _run(exe, tmp_path, x, 50, 0.5, "ab", y)
+    assert rc == 0 and info["join"] == "ab" and info["zone"] == 0
+    ref = oracle_lib.stomp(x, y, 50)
+    assert close(res["mp"], ref[0])[0]
+    assert res["left"].size == 0 and res["right"].size == 0
+
+
+def test_cpp_errors_map_to_reference_exceptions(exe, tmp_path):
+    x = np.cumsum(np.random.default_rng(10).standard_normal(100))
+    rc, info, _ = _run(exe, tmp_path, x, 200, 0.5)
+    assert rc == 2 and info["error"] == "ParameterError"
+    rc, info, _ = _run(exe, tmp_path, x[:3], 4, 0.5)
+    assert rc == 2 and "too short" in info["what"]
