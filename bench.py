@@ -100,23 +100,25 @@ def cpu_sample_rate(cfg, seconds_target=15.0, threads=None):
 
     Returns (unique-cells/s, threads, sample description). Full STOMP rows cost
     L evaluations each and L rows cover the (L-z-1)(L-z)/2 unique cells, so a
-    sample of R rows stands for R/L of the job."""
+    sample of R rows stands for R/L of the job. A 256-row probe sizes the
+    sample to about `seconds_target` seconds."""
     import oracle
     threads = threads or oracle.default_threads()
-    L = cfg.a.size - cfg.window + 1
-    rows = 4096
+    Lrows = (cfg.b.size - cfg.window + 1) if cfg.b is not None else cfg.a.size - cfg.window + 1
+    probe = min(Lrows, 256 * threads)
     t0 = time.perf_counter()
-    oracle.stomp(cfg.a, cfg.b, cfg.window, cfg.ez, n_workers=threads, row_begin=0, row_end=rows)
+    oracle.stomp(cfg.a, cfg.b, cfg.window, cfg.ez, n_workers=threads, row_begin=0, row_end=probe)
     dt = time.perf_counter() - t0
-    if dt < seconds_target / 3:
-        rows = int(min(L, max(rows, rows * seconds_target / max(dt, 1e-3))))
-        rows = max(4096, (rows // 4096) * 4096)
+    rows = int(min(Lrows, max(probe, probe * seconds_target / max(dt, 1e-3))))
+    if rows > probe:
         t0 = time.perf_counter()
         oracle.stomp(cfg.a, cfg.b, cfg.window, cfg.ez, n_workers=threads, row_begin=0, row_end=rows)
         dt = time.perf_counter() - t0
-    Lrows = (cfg.b.size - cfg.window + 1) if cfg.b is not None else L
+    else:
+        rows = probe
     rate = cfg.cells() * (rows / Lrows) / dt
-    return rate, threads, f"oracle STOMP rows [0,{rows}) of {Lrows} ({dt:.1f}s, full rows), extrapolated to unique cells"
+    return rate, threads, (f"oracle STOMP (restated reference) rows [0,{rows}) of {Lrows}, full rows, "
+                           f"{dt:.1f}s on {threads} threads, extrapolated to unique cells")
 
 
 def flush_l2(buf):
@@ -131,7 +133,7 @@ def run_reference(args, cfg, rank, world):
     threads = None
     desc = ""
     for s in range(args.warmup + args.steps):
-        rate, threads, desc = cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
+        rate, threads, desc = cpu_sample_rate(cfg, seconds_target=args.ref_seconds)
         if s >= args.warmup:
             samples.append(rate)
     v = statistics.median(samples)
@@ -154,7 +156,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="cpu_baseline sample length")
+    ap.add_argument("--ref-seconds", type=float, default=4.0, help="--impl reference: per-step sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -167,17 +170,12 @@ def main():
     cfg = datasets.get(args.config)
 
     if args.impl == "reference":
-        if world > 1:
-            import torch.distributed as dist
-            dist.init_process_group("gloo")
-        run_reference(args, cfg, rank, world)
-        if world > 1:
-            import torch.distributed as dist
-            dist.destroy_process_group()
+        run_reference(args, cfg, rank, world)  # rank 0 only; other ranks exit without work
         return
 
     import torch
     import paper_1904_12626_b200 as mp
+    from paper_1904_12626_b200.distributed import merge_keys_
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
@@ -206,8 +204,7 @@ def main():
         if world > 1:
             rk, ck = plan.keys()
             with torch.cuda.stream(stream):
-                dist.all_reduce(rk, op=dist.ReduceOp.MIN)
-                dist.all_reduce(ck, op=dist.ReduceOp.MIN)
+                merge_keys_(rk, ck, root=0)  # NCCL ReduceOp.MIN on the packed int64 keys
         if rank == 0:
             with torch.cuda.stream(stream):
                 outs = plan.outputs()
@@ -332,8 +329,8 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
                 plan.prepare()
                 plan.run(rank, world)
                 rk, ck = plan.keys()
-                dist.all_reduce(rk, op=dist.ReduceOp.MIN)
-                dist.all_reduce(ck, op=dist.ReduceOp.MIN)
+                from paper_1904_12626_b200.distributed import merge_keys_
+                merge_keys_(rk, ck, root=0)
                 if rank == 0:
                     o = plan.outputs()
                     for k, v in o.items():

@@ -243,7 +243,8 @@ int or_stomp(const double *a, int64_t n_a, const double *b, int64_t n_b, int64_t
   if (zone < 0) return -1;
   const int64_t La = n_a - w + 1, Lb = n_b - w + 1;
   if (n_workers < 1) n_workers = 1;
-  if (row_end <= row_begin) { row_begin = 0; row_end = Lb; }
+  const int sample = row_end > row_begin;
+  if (!sample) { row_begin = 0; row_end = Lb; }
   if (row_begin < 0 || row_end > Lb) return -1;
 
   double ga = 0.0, gb = 0.0;
@@ -280,14 +281,21 @@ int or_stomp(const double *a, int64_t n_a, const double *b, int64_t n_b, int64_t
 #else
     const int wk = 0;
 #endif
-    /* Deterministic contiguous chunks, cut on the absolute
-     * 4096-row refresh grid so every row sees the same QT arithmetic for any
-     * n_workers (bit-identical outputs). */
-    const int64_t g0 = row_begin / OR_REFRESH_ROWS;
-    const int64_t nblk = (row_end - 1) / OR_REFRESH_ROWS - g0 + 1;
-    const int64_t b0 = g0 + nblk * wk / n_workers, b1 = g0 + nblk * (wk + 1) / n_workers;
-    const int64_t r0 = imax64(row_begin, b0 * OR_REFRESH_ROWS);
-    const int64_t r1 = imin64(row_end, b1 * OR_REFRESH_ROWS);
+    /* Deterministic contiguous chunks. A full join cuts them on
+     * the absolute 4096-row refresh grid so every row sees the same QT
+     * arithmetic for any n_workers (bit-identical outputs). A
+     * bounded row sample (timing only) splits rows evenly instead. */
+    int64_t r0, r1;
+    if (sample) {
+      r0 = row_begin + (row_end - row_begin) * wk / n_workers;
+      r1 = row_begin + (row_end - row_begin) * (wk + 1) / n_workers;
+    } else {
+      const int64_t g0 = row_begin / OR_REFRESH_ROWS;
+      const int64_t nblk = (row_end - 1) / OR_REFRESH_ROWS - g0 + 1;
+      const int64_t b0 = g0 + nblk * wk / n_workers, b1 = g0 + nblk * (wk + 1) / n_workers;
+      r0 = imax64(row_begin, b0 * OR_REFRESH_ROWS);
+      r1 = imin64(row_end, b1 * OR_REFRESH_ROWS);
+    }
     acc_t A;
     A.v2 = malloc(sizeof(double) * La);
     A.l2 = malloc(sizeof(double) * La);
@@ -300,7 +308,6 @@ int or_stomp(const double *a, int64_t n_a, const double *b, int64_t n_b, int64_t
       A.pi[j] = -1; A.left[j] = -1; A.right[j] = -1;
     }
     double *qt = malloc(sizeof(double) * La), *qn = malloc(sizeof(double) * La);
-    double *d2row = malloc(sizeof(double) * La);
     for (int64_t i = r0; i < r1; ++i) {
       if (i == r0 || i % OR_REFRESH_ROWS == 0) {
         qt_row_direct(bc + i, ac, La, w, qt);
@@ -315,34 +322,31 @@ int or_stomp(const double *a, int64_t n_a, const double *b, int64_t n_b, int64_t
       }
       const double mi = mb[i], si = sb[i];
       const int fi = si == 0.0;
-      if (!fi) {
-        /* distance.hpp:16 with the per-window reciprocals hoisted */
-        const double inv_i = 1.0 / (wd * si), wmi = wd * mi, two_w = 2.0 * wd;
-        for (int64_t j = 0; j < La; ++j) {
-          double d2 = two_w * (1.0 - (qt[j] - wmi * ma[j]) * inv_i * isa[j]);
-          d2 = d2 < 0.0 ? 0.0 : (d2 > 2.0 * two_w ? 2.0 * two_w : d2);
-          if (isa[j] == 0.0) d2 = wd; /* exactly one flat -> sqrt(w) */
-          d2row[j] = d2;
+      /* one fused pass per side: distance (distance.hpp:16 with the per-window
+       * reciprocals hoisted), exclusion zone (distance.hpp:24) by the loop
+       * bounds, merge_min into the profile and into left / right */
+      const double inv_i = fi ? 0.0 : 1.0 / (wd * si), wmi = wd * mi, two_w = 2.0 * wd;
+      const int64_t lo_ex = self ? imax64(0, i - zone) : La, hi_ex = self ? imin64(La - 1, i + zone) : -1;
+      for (int part = 0; part < 2; ++part) {
+        const int64_t j0 = part == 0 ? 0 : (self ? hi_ex + 1 : La);
+        const int64_t j1 = part == 0 ? (self ? lo_ex : La) : La;
+        double *side2 = part == 0 ? A.r2 : A.l2;   /* j < i: row i is a right neighbour of j */
+        int64_t *sidei = part == 0 ? A.right : A.left;
+        for (int64_t j = j0; j < j1; ++j) {
+          double d2;
+          if (!fi) {
+            d2 = two_w * (1.0 - (qt[j] - wmi * ma[j]) * inv_i * isa[j]);
+            d2 = d2 < 0.0 ? 0.0 : (d2 > 2.0 * two_w ? 2.0 * two_w : d2);
+            if (isa[j] == 0.0) d2 = wd; /* exactly one flat -> sqrt(w) */
+          } else {
+            d2 = sa[j] == 0.0 ? 0.0 : wd;
+          }
+          if (d2 < A.v2[j]) { A.v2[j] = d2; A.pi[j] = i; }
+          if (self && d2 < side2[j]) { side2[j] = d2; sidei[j] = i; }
         }
-      } else {
-        for (int64_t j = 0; j < La; ++j) d2row[j] = sa[j] == 0.0 ? 0.0 : wd;
-      }
-      if (self) { /* apply_exclusion_zone_inplace (distance.hpp:24) */
-        const int64_t lo = imax64(0, i - zone), hi = imin64(La - 1, i + zone);
-        for (int64_t j = lo; j <= hi; ++j) d2row[j] = INFINITY;
-      }
-      for (int64_t j = 0; j < La; ++j) {
-        const double d2 = d2row[j];
-        if (d2 < A.v2[j]) { A.v2[j] = d2; A.pi[j] = i; }
-      }
-      if (self) {
-        for (int64_t j = i + 1; j < La; ++j) /* row i is a left neighbour of j > i */
-          if (d2row[j] < A.l2[j]) { A.l2[j] = d2row[j]; A.left[j] = i; }
-        for (int64_t j = 0; j < i && j < La; ++j)
-          if (d2row[j] < A.r2[j]) { A.r2[j] = d2row[j]; A.right[j] = i; }
       }
     }
-    free(qt); free(qn); free(d2row);
+    free(qt); free(qn);
     acc[wk] = A;
   }
   /* Fixed-order merge: worker 0 first, strict improvement. */
