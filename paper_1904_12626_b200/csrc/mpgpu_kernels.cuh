@@ -25,11 +25,20 @@ namespace mpgpu {
 #define MPGPU_D 8
 #endif
 constexpr int kD = MPGPU_D;                // diagonals per thread (register block)
-constexpr int kMinBlocks = kD <= 4 ? 3 : 2;  // CTAs per SM the register budget targets
-constexpr int kWarps = 8;                  // warps per CTA (independent workers)
+#ifndef MPGPU_WARPS
+#define MPGPU_WARPS 8
+#endif
+#ifndef MPGPU_MINBLOCKS
+#define MPGPU_MINBLOCKS 2
+#endif
+constexpr int kMinBlocks = MPGPU_MINBLOCKS;  // CTAs per SM the register budget targets
+constexpr int kWarps = MPGPU_WARPS;          // warps per CTA (independent workers)
 constexpr int kThreads = kWarps * 32;      // 256
 constexpr int kW = 32 * kD;                // diagonals per band = per warp item (256)
-constexpr int kH = 32;                     // rows per warp tile
+#ifndef MPGPU_H
+#define MPGPU_H 32
+#endif
+constexpr int kH = MPGPU_H;                // rows per warp tile
 constexpr int kRing = kW + 2 * kH;         // column ring slots per warp (320)
 constexpr int kNB = kRing / kD;            // blocks per ring plane (40)
 constexpr int kPad = kW + 2 * kH + 64;     // zero padding after the last window
@@ -361,10 +370,20 @@ __device__ __noinline__ SlowOut slow_path(const SlowIn in, unsigned live, int rt
 
 // Any cell over its threshold: hc[d] >= t[d], as a shallow predicate tree
 // (the compiler otherwise chains kD dependent ISETP.OR).
-static_assert(kD == 8, "the hand-unrolled row-steps assume kD == 8");
+static_assert(kD == 8 || kD == 16, "kD must be 8 or 16");
 __device__ __forceinline__ bool any_ge(const int (&hc)[kD], const int (&t)[kD]) {
   unsigned r;
-  if constexpr (kD == 8) {
+  if constexpr (kD == 16) {
+    bool a = false, b = false, c = false, d = false;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      a |= hc[q] >= t[q];
+      b |= hc[4 + q] >= t[4 + q];
+      c |= hc[8 + q] >= t[8 + q];
+      d |= hc[12 + q] >= t[12 + q];
+    }
+    r = (a | b) | (c | d);
+  } else if constexpr (kD == 8) {
     asm("{\n\t.reg .pred a, b, c, d;\n\t"
         "setp.ge.s32 a, %1, %9;\n\t"
         "setp.ge.s32 b, %3, %11;\n\t"
@@ -456,10 +475,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
     }
 
     // ---- tile 0: rows [0, kH) -> buffer 0, columns [0, kH + kW - 1) ------
-    fetch_row(S, PS, 0, lane, r0 + lane);
+    static_assert(kH <= 32, "one row / column per lane per tile");
+    if (lane < kH) fetch_row(S, PS, 0, lane, r0 + lane);
     for (int x = lane; x < kH + kW - 1; x += 32) fetch_col(S, PS, c0, x);
     cp_async_wait_all();
-    fix_row(S, PS, 0, lane, r0 + lane, imask);
+    if (lane < kH) fix_row(S, PS, 0, lane, r0 + lane, imask);
     if (lane == 0) S.rowU[0][0] = make_double2(0.0, 0.0);  // the seed row takes no step
     for (int x = lane; x < kH + kW - 1; x += 32) fix_col(S, PS, c0, x, imask);
     __syncwarp();
@@ -480,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       const int buf = t & 1;
       const long long ts = (long long)t * kH;
       // ---- prefetch tile t+1 (its ring slots held columns retired by now) ----
-      if (t + 1 < nT) {
+      if (t + 1 < nT && lane < kH) {
         fetch_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane);
         fetch_col(S, PS, c0, ts + kH + kW - 1 + lane);
       }
@@ -540,8 +560,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       // ---- land the prefetch (warp-local) -------------------------------------
       if (t + 1 < nT) {
         cp_async_wait_all();
-        fix_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane, imask);
-        fix_col(S, PS, c0, ts + kH + kW - 1 + lane, imask);
+        if (lane < kH) {
+          fix_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane, imask);
+          fix_col(S, PS, c0, ts + kH + kW - 1 + lane, imask);
+        }
       }
       __syncwarp();
     }
