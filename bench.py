@@ -176,12 +176,18 @@ def main():
     import torch
     import paper_1904_12626_b200 as mp
     from paper_1904_12626_b200.distributed import merge_keys_
+    ndev = torch.cuda.device_count()
+    local = local % max(ndev, 1)  # one process per GPU; wraps only in functional tests
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("MPGPU_DIST_BACKEND", "nccl")  # gloo: functional test on 1 GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     stream = torch.cuda.Stream(dev)
     a = torch.from_numpy(cfg.a).to(dev)
