@@ -6,7 +6,7 @@
  * /root/reference/proj/include/mprof/):
  *
  *   mpgpu_join / mpgpu_join_timed  <- mprof::stomp   (profile.hpp:80-83)
- *                                     mprof::scrimp  (profile.hpp:85-89, full run)
+ *   mpgpu_scrimp                   <- mprof::scrimp  (profile.hpp:85-89, incl. anytime s_size)
  *   mpgpu_zone_size                <- mprof::zone_size (distance.hpp:19-20)
  *   mpgpu_rolling_stats            <- mprof::rolling_mean_std (rolling.hpp:25-29)
  *                                     + is_flat_std (rolling.hpp:21-23)
@@ -70,6 +70,22 @@ mpgpu_status mpgpu_join(const mpgpu_join_args *args);
  * the whole call including host<->device copies, in milliseconds. */
 mpgpu_status mpgpu_join_timed(const mpgpu_join_args *args, double *kernel_ms, double *total_ms);
 
+/* SCRIMP (profile.hpp:85-89) with the anytime property: a self-join over a
+ * seeded random subset of diagonal bands (kW = 256 consecutive diagonals each)
+ * covering at least s_size diagonals; s_size <= 0 or >= all diagonals is the
+ * full exact join. *coverage = diagonals computed / all diagonals. Below full
+ * coverage left_a / right_a come back as -1 and values are the
+ * exact minima over the computed diagonals (element-wise upper bounds of the
+ * full profile). AB-joins -> MPGPU_EUNSUPPORTED. */
+mpgpu_status mpgpu_scrimp(const mpgpu_join_args *args, int64_t s_size, uint64_t seed,
+                          double *coverage);
+
+/* The band subset mpgpu_scrimp evaluates for (n, window, zone, s_size, seed):
+ * writes up to `cap` band ids (ascending; band b = diagonals
+ * [zone+1 + 256 b, zone+1 + 256 (b+1))) and returns how many there are. */
+int64_t mpgpu_scrimp_bands(int64_t n, int64_t window, int64_t zone, int64_t s_size, uint64_t seed,
+                           int64_t *out_bands, int64_t cap, double *coverage);
+
 /* Thread-local description of the last failure on this thread. */
 const char *mpgpu_last_error(void);
 
@@ -117,6 +133,15 @@ mpgpu_status mpgpu_plan_keys(mpgpu_plan *plan, int64_t **d_row_keys, int64_t *ro
 mpgpu_status mpgpu_plan_finalize(mpgpu_plan *plan, double *d_mp_a, int64_t *d_pi_a,
                                  int64_t *d_left_a, int64_t *d_right_a, double *d_mp_b,
                                  int64_t *d_pi_b);
+
+/* Anytime mode on a self-join plan: evaluate only the given diagonal bands
+ * (ids as in mpgpu_scrimp_bands); prepare() then skips the warm start and
+ * finalize() searches flat-window candidates band by band. n < 0 or
+ * band_ids == NULL returns the plan to the full join. */
+mpgpu_status mpgpu_plan_select_bands(mpgpu_plan *plan, const int64_t *band_ids, int64_t n);
+
+/* Number of 256-diagonal bands of a self-join plan (0 for AB plans). */
+int64_t mpgpu_plan_num_bands(const mpgpu_plan *plan);
 
 /* Element-wise min of `src` into `dst` (device, same device), for merging
  * shard keys without NCCL. */

@@ -55,6 +55,8 @@ def _load():
                                  ctypes.c_int, ctypes.c_int64, ctypes.c_int64, _dp, _ip, _ip, _ip]
         lib.or_scrimp.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
                                   ctypes.c_uint64, _dp, _ip, _ip, _ip, _dp]
+        lib.or_scrimp_diagonals.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, _ip, ctypes.c_int64,
+                                            _dp, _ip, ctypes.c_int]
         lib.or_apply_exclusion_zone.restype = None
         lib.or_apply_exclusion_zone.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
         lib.or_merge_min.restype = None
@@ -172,6 +174,18 @@ def scrimp(a, w=4, ez=0.5, s_size=0, seed=0):
     if rc:
         raise ValueError("invalid window / fraction")
     return mp, pi, le, ri, cov.value
+
+
+def scrimp_diagonals(a, w, diags, threads=None):
+    """MP / PI over exactly the given diagonals (anytime-run checker)."""
+    a = _f64(a)
+    diags = np.ascontiguousarray(diags, dtype=np.int64)
+    L = a.size - w + 1
+    mp, pi = np.empty(L), np.empty(L, np.int64)
+    if _load().or_scrimp_diagonals(_d(a), a.size, w, _i(diags), diags.size, _d(mp), _i(pi),
+                                   threads or default_threads()):
+        raise ValueError("invalid window")
+    return mp, pi
 
 
 def apply_exclusion_zone(dp, center, zone):

@@ -391,6 +391,66 @@ static uint64_t sm64(uint64_t *s) {
   return z ^ (z >> 31);
 }
 
+/* SCRIMP's inner loop over an explicit list of diagonals: the
+ * checker for partial (anytime) runs whose diagonal subset is known. Values
+ * are the minima over those diagonals only; ties keep the smaller index. */
+int or_scrimp_diagonals(const double *a, int64_t n_a, int64_t w, const int64_t *diags,
+                        int64_t n_diags, double *mp, int64_t *pi, int n_threads) {
+  if (w < 4 || w > n_a) return -1;
+  const int64_t L = n_a - w + 1;
+  double g = 0.0;
+  for (int64_t t = 0; t < n_a; ++t) g += a[t];
+  g /= (double)n_a;
+  double *ac = malloc(sizeof(double) * n_a);
+  for (int64_t t = 0; t < n_a; ++t) ac[t] = a[t] - g;
+  double *mu = malloc(sizeof(double) * L), *sd = malloc(sizeof(double) * L);
+  or_rolling_mean_std(a, n_a, w, mu, sd, n_threads);
+  for (int64_t j = 0; j < L; ++j) mu[j] -= g;
+  for (int64_t j = 0; j < L; ++j) { mp[j] = INFINITY; pi[j] = -1; }
+  /* per-thread accumulators merged in fixed order (ties: smaller index) */
+  if (n_threads < 1) n_threads = 1;
+  double *bv = malloc(sizeof(double) * L * n_threads);
+  int64_t *bi = malloc(sizeof(int64_t) * L * n_threads);
+#pragma omp parallel num_threads(n_threads)
+  {
+#ifdef _OPENMP
+    const int tid = omp_get_thread_num();
+#else
+    const int tid = 0;
+#endif
+    double *v = bv + (size_t)L * tid;
+    int64_t *ix = bi + (size_t)L * tid;
+    for (int64_t j = 0; j < L; ++j) { v[j] = INFINITY; ix[j] = -1; }
+#pragma omp for schedule(dynamic, 8)
+    for (int64_t q = 0; q < n_diags; ++q) {
+      const int64_t k = diags[q];
+      if (k <= 0 || k >= L) continue;
+      double qt = 0.0;
+      for (int64_t t = 0; t < w; ++t) qt += ac[t] * ac[k + t];
+      for (int64_t i = 0; i + k < L; ++i) {
+        const int64_t j = i + k;
+        if (i > 0) qt = qt - ac[i - 1] * ac[j - 1] + ac[i + w - 1] * ac[j + w - 1];
+        if (i > 0 && i % OR_REFRESH_ROWS == 0) {
+          double sacc = 0.0;
+          for (int64_t t = 0; t < w; ++t) sacc += ac[i + t] * ac[j + t];
+          qt = sacc;
+        }
+        const double d = or_znorm_dist_from_qt(qt, w, mu[i], sd[i], mu[j], sd[j]);
+        if (d < v[i] || (d == v[i] && j < ix[i])) { v[i] = d; ix[i] = j; }
+        if (d < v[j] || (d == v[j] && i < ix[j])) { v[j] = d; ix[j] = i; }
+      }
+    }
+  }
+  for (int t = 0; t < n_threads; ++t)
+    for (int64_t j = 0; j < L; ++j) {
+      const double d = bv[(size_t)L * t + j];
+      const int64_t x = bi[(size_t)L * t + j];
+      if (d < mp[j] || (d == mp[j] && x >= 0 && x < pi[j])) { mp[j] = d; pi[j] = x; }
+    }
+  free(bv); free(bi); free(mu); free(sd); free(ac);
+  return 0;
+}
+
 /* scrimp (profile.hpp:85-89): each diagonal's first dot
  * product directly, then the O(1) update along the diagonal; each cell
  * min-merges into row i and row j. */

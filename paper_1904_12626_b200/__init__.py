@@ -23,8 +23,8 @@ import numpy as np
 
 __all__ = [
     "ParameterError", "UnsupportedError", "MatrixProfile", "zone_size", "join_cells",
-    "stomp", "scrimp", "stomp_ab", "join", "Plan", "rolling_stats", "lib", "K_FULL_RUN",
-    "MIN_WINDOW",
+    "stomp", "scrimp", "scrimp_bands", "band_diagonals", "stomp_ab", "join", "Plan",
+    "rolling_stats", "lib", "K_FULL_RUN", "MIN_WINDOW",
 ]
 
 K_FULL_RUN = (1 << 63) - 1   # kFullRun (profile.hpp:20-21)
@@ -105,6 +105,14 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_plan_launch_count.argtypes = [ctypes.c_void_p]
     L.mpgpu_plan_launch_count.restype = ctypes.c_int64
     L.mpgpu_build_info.restype = ctypes.c_char_p
+    L.mpgpu_scrimp.argtypes = [ctypes.POINTER(_JoinArgs), ctypes.c_int64, ctypes.c_uint64, _dp]
+    L.mpgpu_scrimp.restype = ctypes.c_int
+    L.mpgpu_scrimp_bands.argtypes = [ctypes.c_int64] * 4 + [ctypes.c_uint64, _ip, ctypes.c_int64, _dp]
+    L.mpgpu_scrimp_bands.restype = ctypes.c_int64
+    L.mpgpu_plan_select_bands.argtypes = [ctypes.c_void_p, _ip, ctypes.c_int64]
+    L.mpgpu_plan_select_bands.restype = ctypes.c_int
+    L.mpgpu_plan_num_bands.argtypes = [ctypes.c_void_p]
+    L.mpgpu_plan_num_bands.restype = ctypes.c_int64
     _lib = L
     return L
 
@@ -276,15 +284,39 @@ def stomp_ab(ts_a, ts_b, window: int, *, n_gpus: int = 1):
     return pa, pb
 
 
+BAND = 256  # diagonals per band (kW): the granularity of anytime SCRIMP subsets
+
+
+def scrimp_bands(n: int, window: int, zone: int, s_size: int, seed: int = 0):
+    """Band ids (ascending) and coverage of the anytime subset mpgpu_scrimp runs.
+
+    Band b holds diagonals [zone+1 + 256 b, zone+1 + 256 (b+1)), cut at L."""
+    L = n - window + 1
+    nb = max(0, -(-(L - zone - 1) // BAND))
+    out = np.empty(max(nb, 1), np.int64)
+    cov = ctypes.c_double(0)
+    k = lib().mpgpu_scrimp_bands(int(n), int(window), int(zone), int(s_size), ctypes.c_uint64(seed),
+                                 out.ctypes.data_as(_ip), out.size, ctypes.byref(cov))
+    return out[:k].copy(), cov.value
+
+
+def band_diagonals(bands, L: int, zone: int) -> np.ndarray:
+    """Explicit diagonal list of a band subset."""
+    parts = [np.arange(zone + 1 + b * BAND, min(zone + 1 + (b + 1) * BAND, L)) for b in bands]
+    return np.concatenate(parts) if parts else np.empty(0, np.int64)
+
+
 def scrimp(ts_a, window: int = 4, ez_fraction: float = 0.5, s_size: int = K_FULL_RUN,
            seed: int = 0, progress: Optional[Callable[[float], None]] = None,
            ts_b=None) -> MatrixProfile:
-    """mprof::scrimp (profile.hpp:85-89), full coverage, self-join only.
+    """mprof::scrimp (profile.hpp:85-89): self-join with the anytime property.
 
-    An AB-join raises UnsupportedError; an anytime partial run
-    (s_size below the number of diagonals) raises UnsupportedError too — the
-    B200 backend computes the full join, which is what kFullRun asks for.
-    """
+    s_size diagonals (rounded up to whole 256-diagonal bands, chosen in a
+    seeded random order) are evaluated; coverage = computed / all diagonals.
+    At full coverage the result is the exact join with left/right indexes;
+    below it values are exact minima over the computed diagonals and
+    left/right are absent. AB-joins raise
+    UnsupportedError (SPEC.md:219)."""
     if ts_b is not None:
         raise UnsupportedError("SCRIMP supports self-joins only")
     if s_size < 1:
@@ -292,14 +324,33 @@ def scrimp(ts_a, window: int = 4, ez_fraction: float = 0.5, s_size: int = K_FULL
     A = _series(ts_a, "series")
     _check_window(window, A.size, "series")
     zone = zone_size(window, ez_fraction)
-    n_diag = max(0, A.size - window + 1 - zone - 1)
-    if s_size < n_diag:
-        raise UnsupportedError("anytime SCRIMP (s_size < number of diagonals) is not provided "
-                               "by the B200 backend; pass K_FULL_RUN")
-    r = join(A, None, window, zone, progress=progress)
-    return MatrixProfile(values=r["mp_a"], index=r["pi_a"], left_index=r["left_a"],
-                         right_index=r["right_a"], window=window, exclusion_zone=zone,
-                         mode="scrimp", seed=seed, data_len=A.size)
+    L = A.size - window + 1
+    n_diag = max(0, L - zone - 1)
+    if s_size >= n_diag:
+        r = join(A, None, window, zone, progress=progress)
+        return MatrixProfile(values=r["mp_a"], index=r["pi_a"], left_index=r["left_a"],
+                             right_index=r["right_a"], window=window, exclusion_zone=zone,
+                             mode="scrimp", seed=seed, data_len=A.size)
+    mp_a = np.empty(L)
+    pi_a = np.empty(L, np.int64)
+    left = np.empty(L, np.int64)
+    right = np.empty(L, np.int64)
+    args = _JoinArgs()
+    args.a = _ptr(A, _dp)
+    args.n_a = A.size
+    args.window = int(window)
+    args.zone = zone
+    args.n_gpus = 1
+    args.mp_a, args.pi_a = _ptr(mp_a, _dp), _ptr(pi_a, _ip)
+    args.left_a, args.right_a = _ptr(left, _ip), _ptr(right, _ip)
+    cov = ctypes.c_double(0)
+    _check(lib().mpgpu_scrimp(ctypes.byref(args), int(s_size), ctypes.c_uint64(seed), ctypes.byref(cov)))
+    full = cov.value >= 1.0
+    return MatrixProfile(values=mp_a, index=pi_a,
+                         left_index=left if full else np.empty(0, np.int64),
+                         right_index=right if full else np.empty(0, np.int64),
+                         window=window, exclusion_zone=zone, mode="scrimp", coverage=cov.value,
+                         seed=seed, data_len=A.size)
 
 
 # --------------------------------------------------------------- device plans

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <cstdint>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -107,6 +108,10 @@ struct mpgpu_plan {
   int n_ctas = 0;
   long long launches = 0;
   long long seg_rows = 0;
+  // anytime (SCRIMP partial) mode: only these bands (first diagonals, sorted)
+  std::vector<long long> bands;
+  long long* d_bands = nullptr;
+  bool subset = false;
 };
 
 namespace {
@@ -367,6 +372,7 @@ void mpgpu_plan_destroy(mpgpu_plan* p) {
   cudaFree(p->key1);
   cudaFree(p->d_items);
   cudaFree(p->d_counter);
+  cudaFree(p->d_bands);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -382,9 +388,10 @@ mpgpu_status mpgpu_plan_prepare(mpgpu_plan* p) {
   k_fill_keys<<<(unsigned)((p->A.L + 255) / 256), 256, 0, p->stream>>>(p->key0, p->A.L);
   k_fill_keys<<<(unsigned)((L1 + 255) / 256), 256, 0, p->stream>>>(p->key1, L1);
   p->launches += 2;
-  // warm-start keys on a few spread diagonals of every pass
+  // warm-start keys on a few spread diagonals of every pass (full runs only:
+  // an anytime run must not see cells outside its bands)
   JoinParams P = make_params(p);
-  const int npass = p->self ? 1 : 2;
+  const int npass = p->subset ? 0 : (p->self ? 1 : 2);
   for (int q = 0; q < npass; ++q) {
     const Pass& ps = P.pass[q];
     const long long klo = p->self ? p->zone + 1 : (q == 0 ? 0 : 1);
@@ -411,6 +418,12 @@ mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
   MPG_CUDA(cudaSetDevice(p->device));
   std::vector<Item> mine;
   shard_items(p, shard, n_shards, mine, nullptr);
+  if (p->subset) {
+    std::vector<Item> keep;
+    for (const Item& it : mine)
+      if (std::binary_search(p->bands.begin(), p->bands.end(), it.kb)) keep.push_back(it);
+    mine.swap(keep);
+  }
   if (mine.empty()) return MPGPU_OK;
   // each shard uses its own slice of the device item buffer (shards may be
   // in flight together on one device)
@@ -464,7 +477,13 @@ mpgpu_status mpgpu_plan_finalize(mpgpu_plan* p, double* d_mp_a, int64_t* d_pi_a,
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   MPG_CUDA(cudaSetDevice(p->device));
   const int bs = 256;
-  if (p->self) {
+  if (p->self && p->subset) {
+    const long long thr = p->A.L * 32;
+    k_finalize_self_partial<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
+        p->A.view(), p->key0, p->key1, (int)p->m, p->imask, p->d_bands, (int)p->bands.size(),
+        p->A.L, d_mp_a, (long long*)d_pi_a, (long long*)d_left_a, (long long*)d_right_a);
+    p->launches += 1;
+  } else if (p->self) {
     const long long thr = p->A.L * 32;
     k_finalize_self<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
         p->A.view(), p->key0, p->key1, p->zone, (int)p->m, p->imask, d_mp_a,
@@ -486,6 +505,74 @@ mpgpu_status mpgpu_plan_finalize(mpgpu_plan* p, double* d_mp_a, int64_t* d_pi_a,
   }
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
+}
+
+int64_t mpgpu_plan_num_bands(const mpgpu_plan* p) {
+  if (!p || !p->self) return 0;
+  const long long klo = p->zone + 1, L = p->A.L;
+  return L > klo ? (L - klo + kW - 1) / kW : 0;
+}
+
+mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int64_t n) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (n < 0 || !band_ids) {  // back to the full join
+    p->subset = false;
+    p->bands.clear();
+    return MPGPU_OK;
+  }
+  if (!p->self) return fail(MPGPU_EUNSUPPORTED, "band subsets (anytime SCRIMP) are self-join only");
+  const long long nb = mpgpu_plan_num_bands(p), klo = p->zone + 1;
+  std::vector<long long> kb;
+  for (int64_t q = 0; q < n; ++q) {
+    if (band_ids[q] < 0 || band_ids[q] >= nb) return fail(MPGPU_EPARAM, "band id out of range");
+    kb.push_back(klo + band_ids[q] * (long long)kW);
+  }
+  std::sort(kb.begin(), kb.end());
+  kb.erase(std::unique(kb.begin(), kb.end()), kb.end());
+  MPG_CUDA(cudaSetDevice(p->device));
+  cudaFree(p->d_bands);
+  p->d_bands = nullptr;
+  if (!kb.empty()) {
+    MPG_CUDA(cudaMalloc(&p->d_bands, sizeof(long long) * kb.size()));
+    MPG_CUDA(cudaMemcpyAsync(p->d_bands, kb.data(), sizeof(long long) * kb.size(),
+                             cudaMemcpyHostToDevice, p->stream));
+    MPG_CUDA(cudaStreamSynchronize(p->stream));
+  }
+  p->bands.swap(kb);
+  p->subset = true;
+  return MPGPU_OK;
+}
+
+int64_t mpgpu_scrimp_bands(int64_t n, int64_t window, int64_t zone, int64_t s_size, uint64_t seed,
+                           int64_t* out_bands, int64_t cap, double* coverage) {
+  const long long L = n - window + 1, klo = zone + 1;
+  const long long ndiag = L > klo ? L - klo : 0;
+  const long long nb = ndiag > 0 ? (ndiag + kW - 1) / kW : 0;
+  // seeded Fisher-Yates over bands (splitmix64), the band-granular analogue of
+  // SCRIMP's seeded diagonal order
+  std::vector<long long> order(nb);
+  for (long long q = 0; q < nb; ++q) order[q] = q;
+  uint64_t st = seed;
+  auto next = [&st]() {
+    uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  };
+  for (long long q = nb - 1; q > 0; --q) {
+    const long long r = (long long)(next() % (uint64_t)(q + 1));
+    std::swap(order[q], order[r]);
+  }
+  long long covered = 0, take = 0;
+  const long long want = (s_size <= 0 || s_size >= ndiag) ? ndiag : s_size;
+  while (take < nb && covered < want) {
+    const long long b = order[take++];
+    covered += std::min<long long>(kW, ndiag - b * (long long)kW);
+  }
+  std::sort(order.begin(), order.begin() + take);
+  for (long long q = 0; q < take && q < cap; ++q) out_bands[q] = order[q];
+  if (coverage) *coverage = ndiag > 0 ? (double)covered / (double)ndiag : 1.0;
+  return take;
 }
 
 mpgpu_status mpgpu_keys_min_merge(int64_t* d_dst, const int64_t* d_src, int64_t len,
@@ -583,7 +670,8 @@ mpgpu_status ctx_plan(DevCtx* c, const mpgpu_join_args* a) {
   return MPGPU_OK;
 }
 
-mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* total_ms) {
+mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* total_ms,
+                       const std::vector<int64_t>* band_ids = nullptr) {
   const auto t0 = std::chrono::steady_clock::now();
   if (!a || !a->a) return fail(MPGPU_EPARAM, "null arguments");
   const bool self = a->b == nullptr;
@@ -616,6 +704,9 @@ mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* tota
     MPG_CUDA(c->xa.ensure(sizeof(double) * a->n_a));
     if (!self) MPG_CUDA(c->xb.ensure(sizeof(double) * a->n_b));
     st = ctx_plan(c, a);
+    if (st != MPGPU_OK) return st;
+    st = band_ids ? mpgpu_plan_select_bands(c->plan, band_ids->data(), (int64_t)band_ids->size())
+                  : mpgpu_plan_select_bands(c->plan, nullptr, -1);
     if (st != MPGPU_OK) return st;
   }
   for (int g = 0; g < ng; ++g) {
@@ -743,6 +834,25 @@ mpgpu_status mpgpu_join(const mpgpu_join_args* args) { return join_impl(args, nu
 
 mpgpu_status mpgpu_join_timed(const mpgpu_join_args* args, double* kernel_ms, double* total_ms) {
   return join_impl(args, kernel_ms, total_ms);
+}
+
+mpgpu_status mpgpu_scrimp(const mpgpu_join_args* args, int64_t s_size, uint64_t seed,
+                          double* coverage) {
+  if (!args || !args->a) return fail(MPGPU_EPARAM, "null arguments");
+  if (args->b) return fail(MPGPU_EUNSUPPORTED, "SCRIMP supports self-joins only");
+  if (args->window < 4 || args->window > args->n_a)
+    return fail(MPGPU_EPARAM, "window out of range");
+  if (args->zone < 0) return fail(MPGPU_EPARAM, "negative exclusion zone");
+  const long long L = args->n_a - args->window + 1;
+  const long long nb = L > args->zone + 1 ? (L - args->zone - 1 + kW - 1) / kW : 0;
+  std::vector<int64_t> ids((size_t)std::max<long long>(nb, 1));
+  double cov = 1.0;
+  const int64_t n = mpgpu_scrimp_bands(args->n_a, args->window, args->zone, s_size, seed, ids.data(),
+                                       (int64_t)ids.size(), &cov);
+  if (coverage) *coverage = cov;
+  if (cov >= 1.0) return join_impl(args, nullptr, nullptr);  // full coverage: exact join
+  ids.resize((size_t)n);
+  return join_impl(args, nullptr, nullptr, &ids);
 }
 
 }  // extern "C"

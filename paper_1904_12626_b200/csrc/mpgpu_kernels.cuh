@@ -688,6 +688,69 @@ __global__ void k_finalize_self(const Series A, const long long* __restrict__ ke
   }
 }
 
+// Self-join finalize for an anytime (partial) run: only diagonals inside the
+// computed bands [bands[q], bands[q] + kW) count, so the flat-window
+// candidates are searched band by band (SCRIMP partial coverage,
+// SPEC.md:218-223). left/right are absent below full coverage.
+__global__ void k_finalize_self_partial(const Series A, const long long* __restrict__ key_right,
+                                        const long long* __restrict__ key_left, int m,
+                                        long long imask, const long long* __restrict__ bands,
+                                        int n_bands, long long khi, double* __restrict__ mp,
+                                        long long* __restrict__ pi, long long* __restrict__ left,
+                                        long long* __restrict__ right) {
+  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= A.L) return;
+  const long long L = A.L;
+  long long rk = key_right[i], lk = key_left[i];
+  const bool fi = A.inv[i] == 0.0;
+  // right neighbours j = i + k, bands ascending -> j ascending
+  long long rflat = -1, rany = -1;
+  for (int q = 0; q < n_bands && rflat < 0; ++q) {
+    const long long lo = i + bands[q];
+    const long long hi = min(i + min(bands[q] + kW, khi), L);  // exclusive
+    if (lo >= hi) continue;
+    if (rany < 0) rany = lo;
+    const long long f = next_flat(A, lo);
+    if (f >= 0 && f < hi) rflat = f;
+  }
+  // left neighbours j = i - k, bands descending -> j ascending
+  long long lflat = -1, lany = -1;
+  for (int q = n_bands - 1; q >= 0 && lflat < 0; --q) {
+    const long long lo = max(0LL, i - (min(bands[q] + kW, khi) - 1));
+    const long long hi = i - bands[q] + 1;  // exclusive
+    if (lo >= hi) continue;
+    if (lany < 0) lany = lo;
+    const long long f = next_flat(A, lo);
+    if (f >= 0 && f < hi) lflat = f;
+  }
+  if (fi) {
+    rk = rflat >= 0 ? mk_key_score(0.0, rflat, imask)
+                    : (rany >= 0 ? mk_key_score(0.5, rany, imask) : kKeyNone);
+    lk = lflat >= 0 ? mk_key_score(0.0, lflat, imask)
+                    : (lany >= 0 ? mk_key_score(0.5, lany, imask) : kKeyNone);
+  } else {
+    if (rflat >= 0) {
+      const long long k = mk_key_score(0.5, rflat, imask);
+      rk = k < rk ? k : rk;
+    }
+    if (lflat >= 0) {
+      const long long k = mk_key_score(0.5, lflat, imask);
+      lk = k < lk ? k : lk;
+    }
+  }
+  const long long best = lk <= rk ? lk : rk;
+  const long long bi = best == kKeyNone ? -1 : (best & imask);
+  double v = INFINITY;
+  if (bi >= 0) v = convention_or_exact(A, i, A, bi, m, lane);
+  if (lane == 0) {
+    if (mp) mp[i] = v;
+    if (pi) pi[i] = bi;
+    if (left) left[i] = -1;
+    if (right) right[i] = -1;
+  }
+}
+
 // AB-join side: window i of X against every window of Y.
 __global__ void k_finalize_ab(const Series X, const Series Y, const long long* __restrict__ keys,
                               int m, long long imask, double* __restrict__ mp,

@@ -126,12 +126,42 @@ MatrixProfile scrimp(const TimeSeries &ts_a, Index window, double ez_fraction, I
   const Index zone = zone_size(window, ez_fraction);
   const Index L = ts_a.size() - window + 1;
   const Index n_diag = L > zone + 1 ? L - zone - 1 : 0;
-  if (s_size < n_diag)
-    throw UnsupportedError("anytime SCRIMP (s_size < number of diagonals) is not provided by "
-                           "the B200 backend; pass kFullRun");
-  MatrixProfile mp = run_join(ts_a, nullptr, window, zone, progress, false);
+  if (s_size >= n_diag) {  // full run: the exact join
+    MatrixProfile mp = run_join(ts_a, nullptr, window, zone, progress, false);
+    mp.mode = Mode::scrimp;
+    mp.seed = seed;
+    return mp;
+  }
+  // anytime run over a seeded subset of diagonal bands
+  MatrixProfile mp;
+  mp.window = window;
+  mp.exclusion_zone = zone;
   mp.mode = Mode::scrimp;
+  mp.join_kind = JoinKind::self;
   mp.seed = seed;
+  mp.data_len = ts_a.size();
+  mp.values.resize(L);
+  mp.index.resize(L);
+  std::vector<Index> left(L), right(L);
+  mpgpu_join_args args{};
+  args.a = ts_a.values().data();
+  args.n_a = ts_a.size();
+  args.window = window;
+  args.zone = zone;
+  args.n_gpus = 1;
+  args.mp_a = mp.values.data();
+  args.pi_a = mp.index.data();
+  args.left_a = left.data();
+  args.right_a = right.data();
+  double coverage = 0.0;
+  const mpgpu_status st = mpgpu_scrimp(&args, s_size, seed, &coverage);
+  if (st != MPGPU_OK) raise(st);
+  mp.coverage = coverage;
+  if (coverage >= 1.0) {  // left/right only at full coverage
+    mp.left_index.swap(left);
+    mp.right_index.swap(right);
+  }
+  if (progress) progress(1.0);
   return mp;
 }
 

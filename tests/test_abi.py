@@ -78,8 +78,8 @@ def test_parameter_errors_before_device_work(mp):
         mp.stomp(x, None, 10, -0.5)                 # negative zone fraction
     with pytest.raises(mp.UnsupportedError):
         mp.scrimp(x, 10, 0.5, ts_b=x)               # AB-join SCRIMP
-    with pytest.raises(mp.UnsupportedError):
-        mp.scrimp(x, 10, 0.5, s_size=3)             # anytime partial run
+    with pytest.raises(mp.ParameterError):
+        mp.scrimp(x, 10, 0.5, s_size=0)             # s_size < 1
     assert issubclass(mp.UnsupportedError, mp.ParameterError)
     # the C ABI itself rejects bad windows with MPGPU_EPARAM (no device touched)
     args = mp._JoinArgs()
@@ -91,6 +91,23 @@ def test_parameter_errors_before_device_work(mp):
     assert b"window" in mp.lib().mpgpu_last_error()
     p = mp.lib().mpgpu_plan_create(None, 100, None, 0, 8, 4, 0, None)
     assert not p
+
+
+def test_anytime_band_selection_host_logic(mp):
+    n, w = 100000, 256
+    zone = mp.zone_size(w, 0.5)
+    L = n - w + 1
+    nd = L - zone - 1
+    b5, c5 = mp.scrimp_bands(n, w, zone, nd // 20, 7)
+    b20, c20 = mp.scrimp_bands(n, w, zone, nd // 5, 7)
+    assert np.all(np.diff(b5) > 0) and set(b5) <= set(b20)     # same seed: nested subsets
+    assert c5 < c20 < 1.0
+    diags = mp.band_diagonals(b20, L, zone)
+    assert abs(diags.size / nd - c20) < 1e-12 and diags.size >= nd // 5
+    ball, call = mp.scrimp_bands(n, w, zone, 0, 7)
+    assert call == 1.0 and ball.size == -(-nd // 256)
+    b5b, _ = mp.scrimp_bands(n, w, zone, nd // 20, 8)
+    assert not np.array_equal(b5, b5b)                          # the seed matters
 
 
 def test_key_format_mirror():
