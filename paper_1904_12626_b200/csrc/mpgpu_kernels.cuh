@@ -506,9 +506,18 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       }
 
       // ---- compute the tile: kH rows x kD diagonals per lane ----------------
+      // Blocks of kD row-steps run branch-free: each row-step only ORs its
+      // filter result into `anyfire`, so loads and DFMAs of later row-steps
+      // schedule freely across earlier ones. A block in which any lane fired
+      // (a few percent) is replayed from its saved start state with the
+      // per-row-step slow path; the arithmetic of every cell is identical.
       int b0 = (int)((ts / kD + lane) % kNB);
       for (int u = 0; u < kH; u += kD) {
         const int b1 = b0 + 1 == kNB ? 0 : b0 + 1;
+        double covs[kD];
+#pragma unroll
+        for (int d = 0; d < kD; ++d) covs[d] = cov[d];
+        bool anyfire = false;
 #pragma unroll
         for (int s = 0; s < kD; ++s) {
           const int h = u + s;
@@ -523,35 +532,73 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
           const double2 ru = S.rowU[buf][h];
           const double2 ri = S.rowI[buf][h];
           const int rthr = __double2hiint(ri.y);
-          SlowIn in;
           int hcs[kD], tmin[kD];
 #pragma unroll
           for (int d = 0; d < kD; ++d) {
             const int sl = (s + d) % kD;
             cov[d] = fma(ru.x, cU[sl].y, cov[d]);
             cov[d] = fma(ru.y, cU[sl].x, cov[d]);
-            in.c[d] = cov[d] * (ri.x * cinv[sl]);  // rinv*cinv off the cov chain
-            hcs[d] = __double2hiint(in.c[d]);
+            hcs[d] = __double2hiint(cov[d] * (ri.x * cinv[sl]));  // rinv*cinv off the cov chain
             tmin[d] = min(rthr, cthr[sl]);
           }
-          const bool fire = any_ge(hcs, tmin);
+          anyfire |= any_ge(hcs, tmin);
+        }
 #ifdef MPGPU_EXPERIMENT_FASTONLY
-          if (fire && ri.x == 12345.0) {  // never: measures the fast path alone
+        if (anyfire && cov[0] == 12345.0) {  // never: measures the fast blocks alone
 #else
-          if (__builtin_expect(__any_sync(0xffffffffu, fire && ri.x != 0.0), 0)) {
+        if (__builtin_expect(__any_sync(0xffffffffu, anyfire), 0)) {
 #endif
-            unsigned live = 0;
-            if (ri.x != 0.0) {
+          // ---- replay the block with exact key updates -----------------------
 #pragma unroll
-              for (int d = 0; d < kD; ++d) live |= (cinv[(s + d) % kD] != 0.0 ? 1u : 0u) << d;
+          for (int d = 0; d < kD; ++d) cov[d] = covs[d];
+#pragma unroll
+          for (int q = 0; q < kD - 1; ++q) {  // block-start window: columns rho + lane*kD + q
+            const int a = q * kNB + b0;
+            cU[q] = S.colU[a];
+            const double2 ci = S.colI[a];
+            cinv[q] = ci.x;
+            cthr[q] = __double2hiint(ci.y);
+          }
+#pragma unroll
+          for (int s = 0; s < kD; ++s) {
+            const int h = u + s;
+            const int sin = (s + kD - 1) % kD;
+            {
+              const int a = sin * kNB + (s == 0 ? b0 : b1);
+              cU[sin] = S.colU[a];
+              const double2 ci = S.colI[a];
+              cinv[sin] = ci.x;
+              cthr[sin] = __double2hiint(ci.y);
             }
+            const double2 ru = S.rowU[buf][h];
+            const double2 ri = S.rowI[buf][h];
+            const int rthr = __double2hiint(ri.y);
+            SlowIn in;
+            int hcs[kD], tmin[kD];
 #pragma unroll
-            for (int d = 0; d < kD; ++d) in.cthr[d] = cthr[(s + d) % kD];
-            const long long rho = ts + h;
-            const SlowOut o = slow_path(in, live, rthr, r0 + rho, rho + (long long)lane * kD, c0, h,
-                                        buf, imask, PS.keyR, PS.keyC, P.stats);
+            for (int d = 0; d < kD; ++d) {
+              const int sl = (s + d) % kD;
+              cov[d] = fma(ru.x, cU[sl].y, cov[d]);
+              cov[d] = fma(ru.y, cU[sl].x, cov[d]);
+              in.c[d] = cov[d] * (ri.x * cinv[sl]);
+              hcs[d] = __double2hiint(in.c[d]);
+              tmin[d] = min(rthr, cthr[sl]);
+            }
+            const bool fire = any_ge(hcs, tmin);
+            if (__any_sync(0xffffffffu, fire && ri.x != 0.0)) {
+              unsigned live = 0;
+              if (ri.x != 0.0) {
 #pragma unroll
-            for (int d = 0; d < kD; ++d) cthr[(s + d) % kD] = o.cthr[d];
+                for (int d = 0; d < kD; ++d) live |= (cinv[(s + d) % kD] != 0.0 ? 1u : 0u) << d;
+              }
+#pragma unroll
+              for (int d = 0; d < kD; ++d) in.cthr[d] = cthr[(s + d) % kD];
+              const long long rho = ts + h;
+              const SlowOut o = slow_path(in, live, rthr, r0 + rho, rho + (long long)lane * kD, c0,
+                                          h, buf, imask, PS.keyR, PS.keyC, P.stats);
+#pragma unroll
+              for (int d = 0; d < kD; ++d) cthr[(s + d) % kD] = o.cthr[d];
+            }
           }
         }
         b0 = b1;
