@@ -140,6 +140,14 @@ mpgpu_status mpgpu_plan_finalize(mpgpu_plan *plan, double *d_mp_a, int64_t *d_pi
  * band_ids == NULL returns the plan to the full join. */
 mpgpu_status mpgpu_plan_select_bands(mpgpu_plan *plan, const int64_t *band_ids, int64_t n);
 
+/* Point this plan at another plan's keys (mpgpu_plan_keys of the owner),
+ * possibly on a peer device reachable over NVLink: k_join then reads its
+ * filter thresholds from them and RED.MINs its candidates straight into them,
+ * so the cross-device min-merge happens inside the compute (no merge step).
+ * prepare() of an attached plan skips the key initialisation (the owner's
+ * prepare must complete first). NULL, NULL detaches. */
+mpgpu_status mpgpu_plan_attach_keys(mpgpu_plan *plan, int64_t *d_row_keys, int64_t *d_col_keys);
+
 /* Number of 256-diagonal bands of a self-join plan (0 for AB plans). */
 int64_t mpgpu_plan_num_bands(const mpgpu_plan *plan);
 

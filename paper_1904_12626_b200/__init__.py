@@ -111,6 +111,8 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_scrimp_bands.restype = ctypes.c_int64
     L.mpgpu_plan_select_bands.argtypes = [ctypes.c_void_p, _ip, ctypes.c_int64]
     L.mpgpu_plan_select_bands.restype = ctypes.c_int
+    L.mpgpu_plan_attach_keys.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    L.mpgpu_plan_attach_keys.restype = ctypes.c_int
     L.mpgpu_plan_num_bands.argtypes = [ctypes.c_void_p]
     L.mpgpu_plan_num_bands.restype = ctypes.c_int64
     _lib = L
@@ -420,6 +422,12 @@ class Plan:
 
     def launches(self) -> int:
         return int(lib().mpgpu_plan_launch_count(self._p))
+
+    def attach_keys(self, row_keys=None, col_keys=None) -> None:
+        """Evaluate into another plan's keys (e.g. a peer GPU's, over NVLink):
+        candidates are RED.MIN'd straight into them (mpgpu_plan_attach_keys)."""
+        _check(lib().mpgpu_plan_attach_keys(self._p, _dev_ptr(row_keys) or None,
+                                            _dev_ptr(col_keys) or None))
 
     def keys(self):
         """(row_keys, col_keys) as int64 CUDA tensors aliasing the plan's keys."""

@@ -112,6 +112,10 @@ struct mpgpu_plan {
   std::vector<long long> bands;
   long long* d_bands = nullptr;
   bool subset = false;
+  // keys owned by another plan (possibly on a peer device, reached over NVLink):
+  // this plan's k_join reads thresholds from and RED.MINs into them directly
+  long long* ext_key0 = nullptr;
+  long long* ext_key1 = nullptr;
 };
 
 namespace {
@@ -226,23 +230,26 @@ void shard_items(const mpgpu_plan* p, int shard, int n_shards, std::vector<Item>
   if (cells) *cells = c;
 }
 
+long long* key_row(const mpgpu_plan* p) { return p->ext_key0 ? p->ext_key0 : p->key0; }
+long long* key_col(const mpgpu_plan* p) { return p->ext_key1 ? p->ext_key1 : p->key1; }
+
 JoinParams make_params(const mpgpu_plan* p) {
   JoinParams P;
   memset(&P, 0, sizeof(P));
   if (p->self) {
     P.pass[0].R = p->A.view();
     P.pass[0].C = p->A.view();
-    P.pass[0].keyR = p->key0;
-    P.pass[0].keyC = p->key1;
+    P.pass[0].keyR = key_row(p);
+    P.pass[0].keyC = key_col(p);
   } else {
     P.pass[0].R = p->A.view();
     P.pass[0].C = p->B.view();
-    P.pass[0].keyR = p->key0;
-    P.pass[0].keyC = p->key1;
+    P.pass[0].keyR = key_row(p);
+    P.pass[0].keyC = key_col(p);
     P.pass[1].R = p->B.view();
     P.pass[1].C = p->A.view();
-    P.pass[1].keyR = p->key1;
-    P.pass[1].keyC = p->key0;
+    P.pass[1].keyR = key_col(p);
+    P.pass[1].keyC = key_row(p);
   }
   P.m = (int)p->m;
   P.imask = p->imask;
@@ -384,6 +391,10 @@ mpgpu_status mpgpu_plan_prepare(mpgpu_plan* p) {
   mpgpu_status st = launch_stats(p, p->A);
   if (st != MPGPU_OK) return st;
   if (!p->self && (st = launch_stats(p, p->B)) != MPGPU_OK) return st;
+  if (p->ext_key0) {  // keys belong to the owning plan, which initialises them
+    MPG_CUDA(cudaGetLastError());
+    return MPGPU_OK;
+  }
   const long long L1 = p->self ? p->A.L : p->B.L;
   k_fill_keys<<<(unsigned)((p->A.L + 255) / 256), 256, 0, p->stream>>>(p->key0, p->A.L);
   k_fill_keys<<<(unsigned)((L1 + 255) / 256), 256, 0, p->stream>>>(p->key1, L1);
@@ -464,9 +475,9 @@ mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
 mpgpu_status mpgpu_plan_keys(mpgpu_plan* p, int64_t** d_row_keys, int64_t* row_len,
                              int64_t** d_col_keys, int64_t* col_len) {
   if (!p) return fail(MPGPU_EPARAM, "null plan");
-  if (d_row_keys) *d_row_keys = (int64_t*)p->key0;
+  if (d_row_keys) *d_row_keys = (int64_t*)key_row(p);
   if (row_len) *row_len = p->A.L;
-  if (d_col_keys) *d_col_keys = (int64_t*)p->key1;
+  if (d_col_keys) *d_col_keys = (int64_t*)key_col(p);
   if (col_len) *col_len = p->self ? p->A.L : p->B.L;
   return MPGPU_OK;
 }
@@ -511,6 +522,15 @@ int64_t mpgpu_plan_num_bands(const mpgpu_plan* p) {
   if (!p || !p->self) return 0;
   const long long klo = p->zone + 1, L = p->A.L;
   return L > klo ? (L - klo + kW - 1) / kW : 0;
+}
+
+mpgpu_status mpgpu_plan_attach_keys(mpgpu_plan* p, int64_t* d_row_keys, int64_t* d_col_keys) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if ((d_row_keys == nullptr) != (d_col_keys == nullptr))
+    return fail(MPGPU_EPARAM, "attach both key arrays or neither");
+  p->ext_key0 = (long long*)d_row_keys;
+  p->ext_key1 = (long long*)d_col_keys;
+  return MPGPU_OK;
 }
 
 mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int64_t n) {
@@ -709,6 +729,32 @@ mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* tota
                   : mpgpu_plan_select_bands(c->plan, nullptr, -1);
     if (st != MPGPU_OK) return st;
   }
+  DevCtx* c0 = ctx[0];
+  // Fused merge over NVLink: when every shard device can reach device 0's
+  // memory, their k_join instances read thresholds from and RED.MIN straight
+  // into device 0's keys (peer atomics) -- the min-merge happens inside the
+  // compute, no copy or merge kernel. Otherwise: peer copies + k_keys_min.
+  bool fused = ng > 1;
+  for (int g = 1; g < ng && fused; ++g) {
+    DevCtx* c = ctx[g];
+    if (real(c) == real(c0)) continue;
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, real(c), real(c0));
+    if (!can) { fused = false; break; }
+    MPG_CUDA(cudaSetDevice(real(c)));
+    const cudaError_t pe = cudaDeviceEnablePeerAccess(real(c0), 0);
+    if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    else if (pe != cudaSuccess) { cudaGetLastError(); fused = false; }
+  }
+  int64_t *root_r = nullptr, *root_c = nullptr;
+  mpgpu_plan_attach_keys(c0->plan, nullptr, nullptr);
+  mpgpu_plan_keys(c0->plan, &root_r, nullptr, &root_c, nullptr);
+  for (int g = 1; g < ng; ++g) {
+    mpgpu_status st = fused ? mpgpu_plan_attach_keys(ctx[g]->plan, root_r, root_c)
+                            : mpgpu_plan_attach_keys(ctx[g]->plan, nullptr, nullptr);
+    if (st != MPGPU_OK) return st;
+  }
+  cudaEvent_t keys_ready = nullptr;
   for (int g = 0; g < ng; ++g) {
     DevCtx* c = ctx[g];
     MPG_CUDA(cudaSetDevice(real(c)));
@@ -718,8 +764,14 @@ mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* tota
     if (!self)
       MPG_CUDA(cudaMemcpyAsync(c->xb.ptr, a->b, sizeof(double) * a->n_b, cudaMemcpyHostToDevice,
                                c->stream));
-    mpgpu_status st = mpgpu_plan_prepare(c->plan);
+    mpgpu_status st = mpgpu_plan_prepare(c->plan);  // attached plans skip the key init
     if (st != MPGPU_OK) return st;
+    if (g == 0 && fused) {
+      MPG_CUDA(cudaEventCreateWithFlags(&keys_ready, cudaEventDisableTiming));
+      MPG_CUDA(cudaEventRecord(keys_ready, c->stream));
+    } else if (fused) {
+      MPG_CUDA(cudaStreamWaitEvent(c->stream, keys_ready, 0));  // root keys initialised
+    }
     if (!a->progress) {
       st = mpgpu_plan_run(c->plan, g, ng);
       if (st != MPGPU_OK) return st;
@@ -740,31 +792,27 @@ mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* tota
       a->progress((double)(q + 1) / sub, a->progress_ctx);
     }
   }
-  // 2) min-merge shard keys into device 0 (peer copies over NVLink)
-  DevCtx* c0 = ctx[0];
+  // 2) merge: fused -> just order device 0 after every shard; else copy + min
   if (ng > 1) {
-    int64_t *k0r, *k0c;
-    mpgpu_plan_keys(c0->plan, &k0r, nullptr, &k0c, nullptr);
-    MPG_CUDA(cudaSetDevice(real(c0)));
-    MPG_CUDA(c0->keys_in0.ensure(sizeof(long long) * La));
-    MPG_CUDA(c0->keys_in1.ensure(sizeof(long long) * Lb));
+    int64_t *k0r = root_r, *k0c = root_c;
+    if (!fused) {
+      MPG_CUDA(cudaSetDevice(real(c0)));
+      MPG_CUDA(c0->keys_in0.ensure(sizeof(long long) * La));
+      MPG_CUDA(c0->keys_in1.ensure(sizeof(long long) * Lb));
+    }
     for (int g = 1; g < ng; ++g) {
       DevCtx* c = ctx[g];
-      int64_t *kr, *kc;
-      mpgpu_plan_keys(c->plan, &kr, nullptr, &kc, nullptr);
       cudaEvent_t done;
       MPG_CUDA(cudaSetDevice(real(c)));
       MPG_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
       MPG_CUDA(cudaEventRecord(done, c->stream));
       MPG_CUDA(cudaSetDevice(real(c0)));
       MPG_CUDA(cudaStreamWaitEvent(c0->stream, done, 0));
+      cudaEventDestroy(done);
+      if (fused) continue;
+      int64_t *kr, *kc;
+      mpgpu_plan_keys(c->plan, &kr, nullptr, &kc, nullptr);
       if (real(c) != real(c0)) {
-        int can = 0;
-        cudaDeviceCanAccessPeer(&can, real(c0), real(c));
-        if (can) {
-          cudaError_t pe = cudaDeviceEnablePeerAccess(real(c), 0);
-          if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-        }
         MPG_CUDA(cudaMemcpyPeerAsync(c0->keys_in0.ptr, real(c0), kr, real(c),
                                      sizeof(long long) * La, c0->stream));
         MPG_CUDA(cudaMemcpyPeerAsync(c0->keys_in1.ptr, real(c0), kc, real(c),
@@ -780,9 +828,9 @@ mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* tota
       if (st != MPGPU_OK) return st;
       st = mpgpu_keys_min_merge(k0c, (const int64_t*)c0->keys_in1.ptr, Lb, real(c0), c0->stream);
       if (st != MPGPU_OK) return st;
-      cudaEventDestroy(done);
     }
   }
+  if (keys_ready) cudaEventDestroy(keys_ready);
   // 3) finalize on device 0 and copy back
   MPG_CUDA(cudaSetDevice(real(c0)));
   MPG_CUDA(c0->out_mp_a.ensure(sizeof(double) * La));

@@ -139,9 +139,17 @@ def test_virtual_shards_bit_identical(mp):
 
 
 def test_multi_context_join_matches_single(mp):
-    """mpgpu_join with two shards on the same device (peer-merge path)."""
-    x = np.cumsum(np.random.default_rng(21).standard_normal(30000))
+    """mpgpu_join over several shard contexts (fused peer-key merge path; on one
+    GPU the 'peers' are virtual shards on the same device)."""
+    g = np.random.default_rng(21)
+    x = np.cumsum(g.standard_normal(30000))
     r1 = mp.join(x, None, 100, 50)
-    r2 = mp.join(x, None, 100, 50, devices=[0, 0])
-    for k in r1:
-        assert np.array_equal(r1[k], r2[k]), k
+    for devs in ([0, 0], [0, 0, 0]):
+        r2 = mp.join(x, None, 100, 50, devices=devs)
+        for k in r1:
+            assert np.array_equal(r1[k], r2[k]), (devs, k)
+    y = np.cumsum(g.standard_normal(7000))
+    a1 = mp.join(x, y, 64, 0)
+    a2 = mp.join(x, y, 64, 0, devices=[0, 0])
+    for k in a1:
+        assert np.array_equal(a1[k], a2[k]), k
