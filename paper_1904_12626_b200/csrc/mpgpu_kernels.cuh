@@ -514,12 +514,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       int b0 = (int)((ts / kD + lane) % kNB);
       for (int u = 0; u < kH; u += kD) {
         const int b1 = b0 + 1 == kNB ? 0 : b0 + 1;
-#ifdef MPGPU_COVS_LOCAL
-        double covs_mem[kD];  // checkpoint in local memory: 16 registers back to the scheduler
-        volatile double* covs = covs_mem;
-#else
         double covs[kD];
-#endif
 #pragma unroll
         for (int d = 0; d < kD; ++d) covs[d] = cov[d];
         bool anyfire = false;

@@ -1,0 +1,60 @@
+#!/usr/bin/env python3
+"""Per-config numbers for DESIGN.md: GPU join (device-resident), e2e through the
+C ABI, and the CPU oracle STOMP sample, for C1..C5 on one GPU.
+
+    python tools/bench_configs.py [--configs C1,C2,C3,C4,C5] > profiles/configs_r01.jsonl
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1904_12626_b200 as mp  # noqa: E402
+from paper_1904_12626_b200 import datasets  # noqa: E402
+
+sys.path.insert(0, ROOT)
+from bench import cpu_sample_rate  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--configs", default="C1,C2,C3,C4,C5")
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--cpu-seconds", type=float, default=6.0)
+args = ap.parse_args()
+
+for name in args.configs.split(","):
+    cfg = datasets.get(name)
+    a = torch.from_numpy(cfg.a).cuda()
+    b = torch.from_numpy(cfg.b).cuda() if cfg.b is not None else None
+    plan = mp.Plan(a, b, cfg.window, cfg.zone)
+    times = []
+    for r in range(args.reps + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        plan.prepare()
+        plan.run(0, 1)
+        plan.outputs()
+        e1.record()
+        torch.cuda.synchronize()
+        if r:
+            times.append(e0.elapsed_time(e1))
+    ms = min(times)
+    tt = []
+    for r in range(2):
+        out = mp.join(cfg.a, cfg.b, cfg.window, cfg.zone, want_b=cfg.b is not None, timed=True)
+        tt.append(out["total_ms"])
+    cpu, thr, desc = cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
+    line = {"config": name, "workload": cfg.description, "cells": cfg.cells(),
+            "gpu_ms": ms, "gpu_cells_per_s": cfg.cells() / (ms * 1e-3),
+            "e2e_ms": min(tt), "e2e_cells_per_s": cfg.cells() / (min(tt) * 1e-3),
+            "cpu_cells_per_s": cpu, "cpu_threads": thr, "cpu_sample": desc,
+            "speedup_e2e_vs_cpu": cfg.cells() / (min(tt) * 1e-3) / cpu}
+    print(json.dumps(line), flush=True)
+    plan.close()
+    del a, b
+    torch.cuda.empty_cache()
