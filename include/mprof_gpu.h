@@ -106,7 +106,8 @@ mpgpu_status mpgpu_rolling_stats(const double *d_ts, int64_t n, int64_t window, 
 typedef struct mpgpu_plan mpgpu_plan;
 
 /* d_a / d_b: device series on `device` (caller-owned, must outlive the plan);
- * d_b == NULL -> self-join. cuda_stream == NULL -> the plan's own stream. */
+ * d_b == NULL -> self-join. All plan work is issued on cuda_stream (NULL:
+ * the legacy default stream). */
 mpgpu_plan *mpgpu_plan_create(const double *d_a, int64_t n_a, const double *d_b, int64_t n_b,
                               int64_t window, int64_t zone, int32_t device, void *cuda_stream);
 void mpgpu_plan_destroy(mpgpu_plan *plan);

@@ -169,9 +169,14 @@ void build_items(mpgpu_plan* p) {
   }
   // 148 SMs x kMinBlocks CTAs x kWarps warp-workers (fixed: independent of device & shards)
   const long long ref_workers = 148LL * kMinBlocks * kWarps;
-  long long seg = cells / ((long long)kW * 64 * ref_workers);
-  seg = std::max<long long>(kH, std::min<long long>(16384, seg));
-  seg = (seg / kH) * kH;
+  // Segment length: long enough that the kW x m seed each segment pays stays
+  // small (8m rows -> ~6%), short enough that every warp-worker gets at least
+  // two items, and at most 64 items per worker on big joins.
+  const long long seg_balance = cells / ((long long)kW * 64 * ref_workers);
+  const long long seg_fill = cells / ((long long)kW * 2 * ref_workers);
+  long long seg = std::max(seg_balance, std::min<long long>(8 * p->m, seg_fill));
+  seg = std::min<long long>(std::max<long long>(16384, 8 * p->m), seg);
+  seg = std::max<long long>(kH, (seg / kH) * kH);
   p->seg_rows = seg;
 
   p->items.clear();
@@ -315,15 +320,10 @@ mpgpu_plan* mpgpu_plan_create(const double* d_a, int64_t n_a, const double* d_b,
   p->self = d_b == nullptr;
   p->m = window;
   p->zone = p->self ? zone : 0;
-  if (cuda_stream) {
-    p->stream = (cudaStream_t)cuda_stream;
-  } else {
-    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
-      fail(MPGPU_ECUDA, "stream creation failed");
-      return nullptr;
-    }
-    p->own_stream = true;
-  }
+  // NULL is the legacy default stream (CUDA's own convention), so a plan built
+  // on torch's default stream stays ordered with the caller's work
+  p->stream = (cudaStream_t)cuda_stream;
+  p->own_stream = false;
   if (alloc_series(p->A, d_a, n_a, window) != MPGPU_OK) {
     mpgpu_plan_destroy(p.release());
     return nullptr;
@@ -372,7 +372,7 @@ mpgpu_plan* mpgpu_plan_create(const double* d_a, int64_t n_a, const double* d_b,
 void mpgpu_plan_destroy(mpgpu_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
-  if (p->stream) cudaStreamSynchronize(p->stream);
+  cudaStreamSynchronize(p->stream);
   p->A.release();
   p->B.release();
   cudaFree(p->key0);

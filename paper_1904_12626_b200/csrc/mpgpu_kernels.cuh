@@ -438,6 +438,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
     const int nT = it.nrows / kH;
 
     // ---- seeds: cov(r0, r0 + k) for the band's kW diagonals --------------
+    // cov = sum_t a_t (y_t - mu_j) = sum_t a_t y_t - mu_j sum_t a_t with the
+    // row window centred (a_t = x_t - mu_i, sum a_t ~ 0): one DFMA per term.
     double cov[kD];
     {
       double* ac = reinterpret_cast<double*>(S.colU);       // kSeedChunk
@@ -451,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
         mc[e] = j < C.L ? C.mu[j] : 0.0;
         acc[e] = 0.0;
       }
+      double asum = 0.0;
       for (int t0 = 0; t0 < m; t0 += kSeedChunk) {
         const int tc = min(kSeedChunk, m - t0);
         for (int q = lane; q < tc; q += 32) ac[q] = R.x[r0 + t0 + q] - mr;
@@ -461,13 +464,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
         __syncwarp();
         for (int t = 0; t < tc; ++t) {
           const double a = ac[t];
+          asum += a;
 #pragma unroll
-          for (int e = 0; e < kD; ++e) acc[e] = fma(a, xc[lane + e * 32 + t] - mc[e], acc[e]);
+          for (int e = 0; e < kD; ++e) acc[e] = fma(a, xc[lane + e * 32 + t], acc[e]);
         }
         __syncwarp();
       }
 #pragma unroll
-      for (int e = 0; e < kD; ++e) seed[lane + e * 32] = acc[e];
+      for (int e = 0; e < kD; ++e) seed[lane + e * 32] = fma(-mc[e], asum, acc[e]);
       __syncwarp();
 #pragma unroll
       for (int d = 0; d < kD; ++d) cov[d] = seed[lane * kD + d];
