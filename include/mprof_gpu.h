@@ -8,6 +8,7 @@
  *   mpgpu_join / mpgpu_join_timed  <- mprof::stomp   (profile.hpp:80-83)
  *   mpgpu_scrimp                   <- mprof::scrimp  (profile.hpp:85-89, incl. anytime s_size)
  *   mpgpu_zone_size                <- mprof::zone_size (distance.hpp:19-20)
+ *   mpgpu_distance_profiles        <- mprof::mass_distance_profile (distance.hpp:26-33), batched
  *   mpgpu_rolling_stats            <- mprof::rolling_mean_std (rolling.hpp:25-29)
  *                                     + is_flat_std (rolling.hpp:21-23)
  *   mpgpu_plan_*                   <- the stomp worker-chunk contract
@@ -100,6 +101,18 @@ int64_t mpgpu_join_cells(int64_t n_a, int64_t n_b, int64_t window, int64_t zone)
  * windows -> std 0 exactly). d_means / d_stds: device, length n - window + 1. */
 mpgpu_status mpgpu_rolling_stats(const double *d_ts, int64_t n, int64_t window, double *d_means,
                                  double *d_stds, int32_t device, void *cuda_stream);
+
+/* MASS distance-profile batch (mass_distance_profile, distance.hpp:26-33):
+ * n_queries z-normalised distance profiles against every window of the
+ * DEVICE series d_ts, written row-major to d_out[n_queries][n - window + 1].
+ * Queries are either windows of d_ts (d_query_pos, device int64 positions;
+ * |j - pos| <= zone -> +inf, zone < 0: no exclusion) or external device
+ * windows (d_queries, n_queries x window, no exclusion). Exact direct dot
+ * products, flat-window convention, near-zero hits recomputed directly. */
+mpgpu_status mpgpu_distance_profiles(const double *d_ts, int64_t n, int64_t window,
+                                     const double *d_queries, const int64_t *d_query_pos,
+                                     int64_t n_queries, int64_t zone, double *d_out,
+                                     int32_t device, void *cuda_stream);
 
 /* ---- device-resident plan (sharded execution) --------------------------- */
 

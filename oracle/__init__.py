@@ -57,6 +57,8 @@ def _load():
                                   ctypes.c_uint64, _dp, _ip, _ip, _ip, _dp]
         lib.or_scrimp_diagonals.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, _ip, ctypes.c_int64,
                                             _dp, _ip, ctypes.c_int]
+        lib.or_mass_distance_profile.argtypes = [_dp, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64,
+                                                 ctypes.c_int64, _dp, ctypes.c_int]
         lib.or_apply_exclusion_zone.restype = None
         lib.or_apply_exclusion_zone.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
         lib.or_merge_min.restype = None
@@ -186,6 +188,16 @@ def scrimp_diagonals(a, w, diags, threads=None):
                                    threads or default_threads()):
         raise ValueError("invalid window")
     return mp, pi
+
+
+def mass_distance_profile(query, ts, query_index=-1, zone=0, threads=None):
+    """Exact distance profile of one query (mass_distance_profile, distance.hpp:26-33)."""
+    q, ts = _f64(query), _f64(ts)
+    out = np.empty(ts.size - q.size + 1)
+    if _load().or_mass_distance_profile(_d(q), q.size, _d(ts), ts.size, int(query_index), int(zone),
+                                        _d(out), threads or default_threads()):
+        raise ValueError("window out of range")
+    return out
 
 
 def apply_exclusion_zone(dp, center, zone):

@@ -204,6 +204,33 @@ int or_brute_force_rows(const double *a, int64_t n_a, const double *b, int64_t n
   return bad ? -1 : 0;
 }
 
+/* mass_distance_profile (distance.hpp:26-33): distances from a
+ * query window to every window of ts; the FFT dot products are replaced by the
+ * exact direct z-normalised distance (which is also what the reference's
+ * near-zero recompute falls back to). query_index >= 0: |i - query_index| <=
+ * zone -> +inf (self queries, apply_exclusion_zone semantics). */
+int or_mass_distance_profile(const double *query, int64_t w, const double *ts, int64_t n,
+                             int64_t query_index, int64_t zone, double *out, int n_threads) {
+  if (w < 4 || w > n) return -1;
+  const int64_t L = n - w + 1;
+  double qm = 0.0;
+  for (int64_t k = 0; k < w; ++k) qm += query[k];
+  qm /= (double)w;
+  double qss = 0.0;
+  for (int64_t k = 0; k < w; ++k) qss += (query[k] - qm) * (query[k] - qm);
+  double qsd = sqrt(qss / (double)w);
+  if (or_is_flat_std(qsd, qm)) qsd = 0.0;
+  double *mu = malloc(sizeof(double) * L), *sd = malloc(sizeof(double) * L);
+  or_rolling_mean_std(ts, n, w, mu, sd, n_threads);
+#pragma omp parallel for schedule(static) num_threads(n_threads > 0 ? n_threads : 1)
+  for (int64_t i = 0; i < L; ++i) {
+    if (query_index >= 0 && llabs(i - query_index) <= zone) { out[i] = INFINITY; continue; }
+    out[i] = direct_dist(query, qm, qsd, ts + i, mu[i], sd[i], w);
+  }
+  free(mu); free(sd);
+  return 0;
+}
+
 /* ---------------------------------------------------------------- STOMP */
 
 /* Direct QT row: qt[j] = sum_k q[k] * t[j+k] for the (globally centred)

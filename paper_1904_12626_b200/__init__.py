@@ -24,6 +24,7 @@ import numpy as np
 __all__ = [
     "ParameterError", "UnsupportedError", "MatrixProfile", "zone_size", "join_cells",
     "stomp", "scrimp", "scrimp_bands", "band_diagonals", "stomp_ab", "join", "Plan",
+    "distance_profiles", "mass_distance_profile",
     "rolling_stats", "lib", "K_FULL_RUN", "MIN_WINDOW",
 ]
 
@@ -111,6 +112,11 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_scrimp_bands.restype = ctypes.c_int64
     L.mpgpu_plan_select_bands.argtypes = [ctypes.c_void_p, _ip, ctypes.c_int64]
     L.mpgpu_plan_select_bands.restype = ctypes.c_int
+    L.mpgpu_distance_profiles.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                          ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
+                                          ctypes.c_void_p]
+    L.mpgpu_distance_profiles.restype = ctypes.c_int
     L.mpgpu_plan_attach_keys.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     L.mpgpu_plan_attach_keys.restype = ctypes.c_int
     L.mpgpu_plan_num_bands.argtypes = [ctypes.c_void_p]
@@ -460,6 +466,45 @@ class Plan:
         self.finalize(o["mp_a"], o["pi_a"], o.get("left_a"), o.get("right_a"), o.get("mp_b"),
                       o.get("pi_b"))
         return o
+
+
+def distance_profiles(ts, window: int, queries=None, positions=None, zone: int = -1, stream=None):
+    """MASS distance-profile batch on the GPU (mass_distance_profile, distance.hpp:26-33).
+
+    ts: float64 CUDA tensor. Either `queries` (Q x window float64 CUDA tensor,
+    external windows) or `positions` (Q int64 CUDA tensor of window starts in
+    ts; |j - pos| <= zone -> +inf, zone < 0: none). Returns a Q x L tensor."""
+    import torch
+    _check_window(window, ts.numel(), "series")
+    L = ts.numel() - window + 1
+    if (queries is None) == (positions is None):
+        raise ParameterError("pass exactly one of queries / positions")
+    Q = queries.shape[0] if queries is not None else positions.numel()
+    if queries is not None and (queries.dim() != 2 or queries.shape[1] != window):
+        raise ParameterError("queries must be Q x window")
+    out = torch.empty((Q, L), dtype=torch.float64, device=ts.device)
+    st = stream if stream is not None else torch.cuda.current_stream(ts.device)
+    _check(lib().mpgpu_distance_profiles(
+        _dev_ptr(ts), ts.numel(), int(window),
+        _dev_ptr(queries.contiguous()) if queries is not None else None,
+        _dev_ptr(positions.contiguous()) if positions is not None else None,
+        int(Q), int(zone), _dev_ptr(out), ts.device.index or 0, ctypes.c_void_p(st.cuda_stream)))
+    return out
+
+
+def mass_distance_profile(query, ts, query_index: int = -1, ez_zone: int = 0) -> np.ndarray:
+    """Host mirror of mprof::mass_distance_profile (distance.hpp:30-33) on the GPU."""
+    import torch
+    q = _series(query, "query")
+    t = _series(ts, "series")
+    _check_window(q.size, t.size, "series")
+    d = torch.from_numpy(t).cuda()
+    if query_index >= 0:
+        out = distance_profiles(d, q.size, positions=torch.tensor([query_index], device=d.device),
+                                zone=ez_zone)
+    else:
+        out = distance_profiles(d, q.size, queries=torch.from_numpy(q).cuda().view(1, -1))
+    return out[0].cpu().numpy()
 
 
 def rolling_stats(ts, window: int, stream=None):

@@ -595,6 +595,32 @@ int64_t mpgpu_scrimp_bands(int64_t n, int64_t window, int64_t zone, int64_t s_si
   return take;
 }
 
+mpgpu_status mpgpu_distance_profiles(const double* d_ts, int64_t n, int64_t window,
+                                     const double* d_queries, const int64_t* d_query_pos,
+                                     int64_t n_queries, int64_t zone, double* d_out,
+                                     int32_t device, void* cuda_stream) {
+  if (!d_ts || !d_out || window < 4 || window > n) return fail(MPGPU_EPARAM, "window out of range");
+  if ((d_queries == nullptr) == (d_query_pos == nullptr))
+    return fail(MPGPU_EPARAM, "pass exactly one of query arrays or query positions");
+  if (n_queries <= 0) return MPGPU_OK;
+  if (n_queries > 65535) return fail(MPGPU_EPARAM, "at most 65535 queries per call");
+  MPG_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const long long L = n - window + 1;
+  double *mu = nullptr, *inv = nullptr;
+  MPG_CUDA(cudaMallocAsync(&mu, sizeof(double) * L, st));
+  MPG_CUDA(cudaMallocAsync(&inv, sizeof(double) * L, st));
+  k_window_stats<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(d_ts, L, (int)window, mu, inv,
+                                                              nullptr, nullptr);
+  dim3 grid((unsigned)((L + kMassTile - 1) / kMassTile), (unsigned)n_queries);
+  k_mass<<<grid, kMassThreads, 0, st>>>(d_ts, n, mu, inv, L, (int)window, d_queries,
+                                        (const long long*)d_query_pos, zone < 0 ? -1 : zone, d_out);
+  MPG_CUDA(cudaGetLastError());
+  MPG_CUDA(cudaFreeAsync(mu, st));
+  MPG_CUDA(cudaFreeAsync(inv, st));
+  return MPGPU_OK;
+}
+
 mpgpu_status mpgpu_keys_min_merge(int64_t* d_dst, const int64_t* d_src, int64_t len,
                                   int32_t device, void* cuda_stream) {
   MPG_CUDA(cudaSetDevice(device));

@@ -652,6 +652,108 @@ __global__ void k_init_keys(const Pass PS, long long klo, long long khi, int m, 
   red_min(&PS.keyC[j], mk_key(c, i, imask));
 }
 
+// ---- K6: distance-profile batch (MASS, distance.hpp:26-33) --------------------
+// Q query windows against every window of a series: out[q][j] = z-normalised
+// distance, flat-window convention, |j - pos_q| <= zone -> +inf for queries
+// taken from the series itself. Direct centred dot products (exact; no FFT):
+// cov = sum_t a_t x_{j+t} - mu_j sum_t a_t with a = query - mean(query).
+// Each CTA owns one query and a span of kMassTile outputs; each thread owns
+// kMassR consecutive outputs and slides a register window over the staged
+// series (1 shared load per kMassR DFMAs). Near-zero hits are recomputed
+// directly so exact matches come out as 0 (distance.hpp:30-33).
+constexpr int kMassThreads = 128;
+constexpr int kMassR = 8;
+constexpr int kMassTile = kMassThreads * kMassR;  // outputs per CTA (1024)
+constexpr int kMassChunk = 512;                   // query samples staged per pass
+
+__global__ void __launch_bounds__(kMassThreads) k_mass(
+    const double* __restrict__ x, long long n, const double* __restrict__ mu,
+    const double* __restrict__ inv, long long L, int m, const double* __restrict__ queries,
+    const long long* __restrict__ qpos, long long zone, double* __restrict__ out) {
+  __shared__ double sq[kMassChunk];
+  __shared__ double sx[kMassTile + kMassChunk];
+  __shared__ double qstat[2];
+  const int q = blockIdx.y;
+  const long long j0 = (long long)blockIdx.x * kMassTile;
+  const int tid = threadIdx.x;
+  const double* qx = queries ? queries + (long long)q * m : x + qpos[q];
+  // query mean and inverse norm: the same sequential two-pass as K1, so a query
+  // equal to a window of the series gets bit-identical statistics (exact 0)
+  if (tid == 0) {
+    double s = 0.0;
+    for (int t = 0; t < m; ++t) s += qx[t];
+    const double mean = s / (double)m;
+    double ss = 0.0;
+    for (int t = 0; t < m; ++t) {
+      const double d = qx[t] - mean;
+      ss = fma(d, d, ss);
+    }
+    const double sd = sqrt(ss / (double)m);
+    const double scale = fabs(mean) > 1.0 ? fabs(mean) : 1.0;
+    qstat[0] = mean;
+    qstat[1] = sd <= 1e-10 * scale ? 0.0 : 1.0 / sqrt(ss);
+  }
+  __syncthreads();
+  const double qmean = qstat[0], qinv = qstat[1];
+  double acc[kMassR];
+#pragma unroll
+  for (int r = 0; r < kMassR; ++r) acc[r] = 0.0;
+  double asum = 0.0;
+  const int jl = tid * kMassR;  // first local output of this thread
+  for (int t0 = 0; t0 < m; t0 += kMassChunk) {
+    const int tc = min(kMassChunk, m - t0);
+    for (int t = tid; t < tc; t += kMassThreads) sq[t] = qx[t0 + t] - qmean;
+    for (int t = tid; t < kMassTile + tc; t += kMassThreads) {
+      const long long g = j0 + t0 + t;
+      sx[t] = g < n ? x[g] : 0.0;
+    }
+    __syncthreads();
+    double w[kMassR];
+#pragma unroll
+    for (int r = 0; r < kMassR; ++r) w[r] = sx[jl + r];
+    for (int t = 0; t < tc; ++t) {
+      const double a = sq[t];
+      asum += a;
+#pragma unroll
+      for (int r = 0; r < kMassR; ++r) acc[r] = fma(a, w[r], acc[r]);
+#pragma unroll
+      for (int r = 0; r < kMassR - 1; ++r) w[r] = w[r + 1];
+      w[kMassR - 1] = sx[jl + kMassR + t];
+    }
+    __syncthreads();
+  }
+  const long long p = qpos ? qpos[q] : -1;
+#pragma unroll
+  for (int r = 0; r < kMassR; ++r) {
+    const long long j = j0 + jl + r;
+    if (j >= L) break;
+    double d;
+    const double ij = inv[j];
+    if (p >= 0 && llabs(j - p) <= zone) {
+      d = INFINITY;
+    } else if (qinv == 0.0 || ij == 0.0) {
+      d = (qinv == 0.0 && ij == 0.0) ? 0.0 : sqrt((double)m);
+    } else {
+      const double corr = fma(-mu[j], asum, acc[r]) * (qinv * ij);
+      double d2 = 2.0 * m * (1.0 - corr);
+      if (d2 < 1e-6) {  // near-zero hit: recompute directly (distance.hpp:30-33)
+        const double* xj = x + j;
+        const double mj = mu[j];
+        double e = 0.0;
+        for (int t = 0; t < m; ++t) {
+          // rounded products (no FMA contraction): identical windows give exactly 0
+          const double u = __dmul_rn(qx[t] - qmean, qinv) - __dmul_rn(xj[t] - mj, ij);
+          e = fma(u, u, e);
+        }
+        d2 = (double)m * e;
+      }
+      d2 = d2 < 0.0 ? 0.0 : (d2 > 4.0 * m ? 4.0 * m : d2);
+      d = sqrt(d2);
+    }
+    out[(long long)q * L + j] = d;
+  }
+}
+
 // ---- K5: key merge -------------------------------------------------------------
 __global__ void k_keys_min(long long* __restrict__ dst, const long long* __restrict__ src,
                            long long len) {
@@ -677,7 +779,8 @@ __device__ __forceinline__ double warp_exact_dist(const Series& X, long long i, 
   const double* yj = Y.x + j;
   double acc = 0.0;
   for (int t = lane; t < m; t += 32) {
-    const double d = (xi[t] - mi) * ii - (yj[t] - mj) * ij;
+    // rounded products (no FMA contraction): identical windows give exactly 0
+    const double d = __dmul_rn(xi[t] - mi, ii) - __dmul_rn(yj[t] - mj, ij);
     acc = fma(d, d, acc);
   }
 #pragma unroll
