@@ -9,6 +9,8 @@
  *   mpgpu_scrimp                   <- mprof::scrimp  (profile.hpp:85-89, incl. anytime s_size)
  *   mpgpu_zone_size                <- mprof::zone_size (distance.hpp:19-20)
  *   mpgpu_distance_profiles        <- mprof::mass_distance_profile (distance.hpp:26-33), batched
+ *   mpgpu_fluss / mpgpu_extract    <- fluss_arc_count / fluss_cac / fluss_extract / find_discord
+ *                                     (discovery.hpp:61-79)
  *   mpgpu_rolling_stats            <- mprof::rolling_mean_std (rolling.hpp:25-29)
  *                                     + is_flat_std (rolling.hpp:21-23)
  *   mpgpu_plan_*                   <- the stomp worker-chunk contract
@@ -113,6 +115,23 @@ mpgpu_status mpgpu_distance_profiles(const double *d_ts, int64_t n, int64_t wind
                                      const double *d_queries, const int64_t *d_query_pos,
                                      int64_t n_queries, int64_t zone, double *d_out,
                                      int32_t device, void *cuda_stream);
+
+/* FLUSS on the GPU (fluss_arc_count + fluss_cac, discovery.hpp:68-74): arc
+ * counts from a device profile index (d_arcs[L], int64) and, if d_cac is not
+ * NULL, the corrected arc curve (d_cac[L], 1 within `window` of either end). */
+mpgpu_status mpgpu_fluss(const int64_t *d_index, int64_t L, int64_t window, int64_t *d_arcs,
+                         double *d_cac, int32_t device, void *cuda_stream);
+
+/* Repeated arg-extreme extraction with a +-zone mask around every pick, on a
+ * DEVICE array: largest != 0 -> discords (find_discord, discovery.hpp:61-63,
+ * stops when the max <= stop_at, pass -inf for no stop); largest == 0 ->
+ * minima (fluss_extract, discovery.hpp:76-79, stops once the min >= stop_at,
+ * 1.0 for FLUSS). Non-finite entries never qualify; ties -> smallest index.
+ * Writes up to k host indexes (and values) and returns how many were found,
+ * -1 on error. */
+int64_t mpgpu_extract(const double *d_values, int64_t n, int64_t k, int64_t zone, int32_t largest,
+                      double stop_at, int64_t *out_index, double *out_value, int32_t device,
+                      void *cuda_stream);
 
 /* ---- device-resident plan (sharded execution) --------------------------- */
 

@@ -226,3 +226,57 @@ def ref_timeseries_validate(x):
     buf = ctypes.create_string_buffer(256)
     rc = _ref.ref_timeseries_validate(_d(x), x.size, buf, 256)
     return rc, buf.value.decode()
+
+
+# ---------------------------------------------------------------- MP consumers
+# numpy restatements of discovery.hpp:61-79 (checkers for the GPU versions).
+
+def fluss_arc_count(index):
+    """arc_counts[i] = number of nearest-neighbour arcs strictly crossing i
+    (discovery.hpp:68-70), via a +1/-1 sweep."""
+    index = np.asarray(index, dtype=np.int64)
+    L = index.size
+    i = np.arange(L)
+    ok = (index >= 0) & (index < L) & (index != i)
+    lo = np.minimum(i, index)[ok]
+    hi = np.maximum(i, index)[ok]
+    keep = hi - lo >= 2
+    diff = np.zeros(L + 1, np.int64)
+    np.add.at(diff, lo[keep] + 1, 1)
+    np.add.at(diff, hi[keep], -1)
+    return np.cumsum(diff[:L])
+
+
+def fluss_cac(arcs, window):
+    """Corrected arc curve (discovery.hpp:72-74)."""
+    arcs = np.asarray(arcs, dtype=np.float64)
+    L = arcs.size
+    i = np.arange(L, dtype=np.float64)
+    ideal = 2.0 * i * (L - i) / L
+    with np.errstate(divide="ignore", invalid="ignore"):
+        cac = np.where(ideal > 0, arcs / ideal, 1.0)
+    cac = np.clip(cac, 0.0, 1.0)
+    cac[:window] = 1.0
+    cac[max(0, L - window):] = 1.0
+    return cac
+
+
+def extract(values, k, zone, largest, stop_at):
+    """Repeated arg-extreme with +-zone masking (find_discord / fluss_extract)."""
+    v = np.array(values, dtype=np.float64)
+    out = []
+    for _ in range(k):
+        fin = np.isfinite(v)
+        if not fin.any():
+            break
+        if largest:
+            j = int(np.argmax(np.where(fin, v, -np.inf)))
+            if not v[j] > stop_at:
+                break
+        else:
+            j = int(np.argmin(np.where(fin, v, np.inf)))
+            if not v[j] < stop_at:
+                break
+        out.append((j, float(v[j])))
+        v[max(0, j - zone):j + zone + 1] = np.inf if not largest else -np.inf
+    return out

@@ -24,7 +24,7 @@ import numpy as np
 __all__ = [
     "ParameterError", "UnsupportedError", "MatrixProfile", "zone_size", "join_cells",
     "stomp", "scrimp", "scrimp_bands", "band_diagonals", "stomp_ab", "join", "Plan",
-    "distance_profiles", "mass_distance_profile",
+    "distance_profiles", "mass_distance_profile", "find_discord", "fluss", "fluss_extract",
     "rolling_stats", "lib", "K_FULL_RUN", "MIN_WINDOW",
 ]
 
@@ -117,6 +117,13 @@ def lib() -> ctypes.CDLL:
                                           ctypes.c_int64, ctypes.c_void_p, ctypes.c_int32,
                                           ctypes.c_void_p]
     L.mpgpu_distance_profiles.restype = ctypes.c_int
+    L.mpgpu_fluss.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                              ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]
+    L.mpgpu_fluss.restype = ctypes.c_int
+    L.mpgpu_extract.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                ctypes.c_int32, ctypes.c_double, _ip, _dp, ctypes.c_int32,
+                                ctypes.c_void_p]
+    L.mpgpu_extract.restype = ctypes.c_int64
     L.mpgpu_plan_attach_keys.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     L.mpgpu_plan_attach_keys.restype = ctypes.c_int
     L.mpgpu_plan_num_bands.argtypes = [ctypes.c_void_p]
@@ -505,6 +512,57 @@ def mass_distance_profile(query, ts, query_index: int = -1, ez_zone: int = 0) ->
     else:
         out = distance_profiles(d, q.size, queries=torch.from_numpy(q).cuda().view(1, -1))
     return out[0].cpu().numpy()
+
+
+def _extract(d_values, k, zone, largest, stop_at):
+    import torch
+    idx = np.empty(max(int(k), 1), np.int64)
+    val = np.empty(max(int(k), 1))
+    st = torch.cuda.current_stream(d_values.device)
+    got = lib().mpgpu_extract(_dev_ptr(d_values), d_values.numel(), int(k), int(zone), int(largest),
+                              float(stop_at), idx.ctypes.data_as(_ip), val.ctypes.data_as(_dp),
+                              d_values.device.index or 0, ctypes.c_void_p(st.cuda_stream))
+    if got < 0:
+        _check(MPGPU_EPARAM)
+    return idx[:got].copy(), val[:got].copy()
+
+
+def find_discord(profile: MatrixProfile, n_discords: int, zone: int = -1):
+    """find_discord (discovery.hpp:61-63) on the GPU: repeated argmax of the
+    finite profile values, masking +-zone around each hit (zone < 0: the
+    profile's own exclusion zone). Returns (list of (index, distance), truncated)."""
+    import torch
+    if n_discords < 0:
+        raise ParameterError("n_discords must be >= 0")
+    z = profile.exclusion_zone if zone < 0 else int(zone)
+    d = torch.from_numpy(np.ascontiguousarray(profile.values, dtype=np.float64)).cuda()
+    idx, val = _extract(d, n_discords, z, True, -np.inf)
+    return list(zip(idx.tolist(), val.tolist())), bool(idx.size < n_discords)
+
+
+def fluss(profile_index, window: int):
+    """fluss_arc_count + fluss_cac (discovery.hpp:68-74) on the GPU.
+    Returns (arc_counts int64, cac float64) as numpy arrays."""
+    import torch
+    ix = torch.from_numpy(np.ascontiguousarray(profile_index, dtype=np.int64)).cuda()
+    L = ix.numel()
+    arcs = torch.empty(L, dtype=torch.int64, device=ix.device)
+    cac = torch.empty(L, dtype=torch.float64, device=ix.device)
+    st = torch.cuda.current_stream(ix.device)
+    _check(lib().mpgpu_fluss(_dev_ptr(ix), L, int(window), _dev_ptr(arcs), _dev_ptr(cac),
+                             ix.device.index or 0, ctypes.c_void_p(st.cuda_stream)))
+    return arcs.cpu().numpy(), cac.cpu().numpy()
+
+
+def fluss_extract(cac, num_segments: int, window: int, exclusion_factor: float = 5.0):
+    """fluss_extract (discovery.hpp:76-79): repeated argmin over the CAC, masking
+    +-exclusion_factor*window, stopping once nothing below 1 remains.
+    Returns (segment positions, truncated)."""
+    import torch
+    c = torch.from_numpy(np.ascontiguousarray(cac, dtype=np.float64)).cuda()
+    zone = int(np.floor(exclusion_factor * window))
+    idx, _ = _extract(c, num_segments, zone, False, 1.0)
+    return idx.tolist(), bool(idx.size < num_segments)
 
 
 def rolling_stats(ts, window: int, stream=None):

@@ -621,6 +621,80 @@ mpgpu_status mpgpu_distance_profiles(const double* d_ts, int64_t n, int64_t wind
   return MPGPU_OK;
 }
 
+namespace {
+// arg-extreme of a device array: two-level block reduction; result to host
+mpgpu_status argext(const double* d_v, long long n, int sign, cudaStream_t st, double* tmp_v,
+                    long long* tmp_i, double* val, long long* idx) {
+  const int bs = 1024;
+  long long nb = (n + bs - 1) / bs;
+  k_argext<<<(unsigned)nb, bs, 0, st>>>(d_v, nullptr, n, sign, tmp_v, tmp_i);
+  while (nb > 1) {
+    const long long nb2 = (nb + bs - 1) / bs;
+    k_argext<<<(unsigned)nb2, bs, 0, st>>>(tmp_v, tmp_i, nb, sign, tmp_v + nb, tmp_i + nb);
+    MPG_CUDA(cudaMemcpyAsync(tmp_v, tmp_v + nb, sizeof(double) * nb2, cudaMemcpyDeviceToDevice, st));
+    MPG_CUDA(cudaMemcpyAsync(tmp_i, tmp_i + nb, sizeof(long long) * nb2, cudaMemcpyDeviceToDevice, st));
+    nb = nb2;
+  }
+  MPG_CUDA(cudaMemcpyAsync(val, tmp_v, sizeof(double), cudaMemcpyDeviceToHost, st));
+  MPG_CUDA(cudaMemcpyAsync(idx, tmp_i, sizeof(long long), cudaMemcpyDeviceToHost, st));
+  MPG_CUDA(cudaStreamSynchronize(st));
+  return MPGPU_OK;
+}
+}  // namespace
+
+mpgpu_status mpgpu_fluss(const int64_t* d_index, int64_t L, int64_t window, int64_t* d_arcs,
+                         double* d_cac, int32_t device, void* cuda_stream) {
+  if (!d_index || !d_arcs || L < 1 || window < 0) return fail(MPGPU_EPARAM, "bad FLUSS arguments");
+  MPG_CUDA(cudaSetDevice(device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  MPG_CUDA(cudaMemsetAsync(d_arcs, 0, sizeof(long long) * L, st));
+  k_arc_ends<<<(unsigned)((L + 255) / 256), 256, 0, st>>>((const long long*)d_index, L,
+                                                         (long long*)d_arcs);
+  k_scan_inclusive<<<1, 1024, 0, st>>>((long long*)d_arcs, L);
+  if (d_cac)
+    k_cac<<<(unsigned)((L + 255) / 256), 256, 0, st>>>((const long long*)d_arcs, L, window, d_cac);
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+int64_t mpgpu_extract(const double* d_values, int64_t n, int64_t k, int64_t zone, int32_t largest,
+                      double stop_at, int64_t* out_index, double* out_value, int32_t device,
+                      void* cuda_stream) {
+  if (!d_values || n < 1 || k < 0 || zone < 0) { fail(MPGPU_EPARAM, "bad extract arguments"); return -1; }
+  if (cudaSetDevice(device) != cudaSuccess) { fail(MPGPU_ECUDA, "cudaSetDevice"); return -1; }
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  double* v = nullptr;
+  double* tv = nullptr;
+  long long* ti = nullptr;
+  const long long nb = (n + 1023) / 1024;
+  if (cudaMallocAsync(&v, sizeof(double) * n, st) != cudaSuccess ||
+      cudaMallocAsync(&tv, sizeof(double) * 2 * (nb + 2), st) != cudaSuccess ||
+      cudaMallocAsync(&ti, sizeof(long long) * 2 * (nb + 2), st) != cudaSuccess) {
+    fail(MPGPU_ENOMEM, "extract scratch");
+    return -1;
+  }
+  cudaMemcpyAsync(v, d_values, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+  const int sign = largest ? 1 : -1;
+  const double masked = largest ? -INFINITY : INFINITY;  // masked entries are non-finite: skipped
+  int64_t found = 0;
+  for (; found < k; ++found) {
+    double val;
+    long long idx;
+    if (argext(v, n, sign, st, tv, ti, &val, &idx) != MPGPU_OK || idx < 0) break;
+    if (!largest && val >= stop_at) break;   // FLUSS: nothing below the stop value remains
+    if (largest && val <= stop_at) break;
+    out_index[found] = idx;
+    if (out_value) out_value[found] = val;
+    const long long span = 2 * zone + 1;
+    k_mask_zone<<<(unsigned)((span + 255) / 256), 256, 0, st>>>(v, n, idx, zone, masked);
+  }
+  cudaFreeAsync(v, st);
+  cudaFreeAsync(tv, st);
+  cudaFreeAsync(ti, st);
+  cudaStreamSynchronize(st);
+  return found;
+}
+
 mpgpu_status mpgpu_keys_min_merge(int64_t* d_dst, const int64_t* d_src, int64_t len,
                                   int32_t device, void* cuda_stream) {
   MPG_CUDA(cudaSetDevice(device));

@@ -754,6 +754,117 @@ __global__ void __launch_bounds__(kMassThreads) k_mass(
   }
 }
 
+// ---- K7: matrix-profile consumers (discovery.hpp:61-79) -----------------------
+// FLUSS arc count: every nearest-neighbour arc (i, index[i]) adds +1 on the open
+// interval strictly between its endpoints (a +1/-1 sweep, discovery.hpp:68-70).
+__global__ void k_arc_ends(const long long* __restrict__ index, long long L,
+                           long long* __restrict__ diff) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= L) return;
+  const long long j = index[i];
+  if (j < 0 || j >= L || j == i) return;
+  const long long lo = i < j ? i : j, hi = i < j ? j : i;
+  if (hi - lo < 2) return;
+  atomicAdd((unsigned long long*)&diff[lo + 1], 1ull);
+  atomicAdd((unsigned long long*)&diff[hi], (unsigned long long)-1LL);
+}
+
+// Inclusive prefix sum in one block (L up to a few 1e7): per-thread chunk sums,
+// a block scan of the chunk totals, then the chunk rewrite.
+__global__ void k_scan_inclusive(long long* __restrict__ a, long long L) {
+  __shared__ long long tot[1024];
+  const int t = threadIdx.x, nt = blockDim.x;
+  const long long chunk = (L + nt - 1) / nt;
+  const long long lo = t * chunk, hi = lo + chunk < L ? lo + chunk : L;
+  long long s = 0;
+  for (long long i = lo; i < hi; ++i) s += a[i];
+  tot[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    long long run = 0;
+    for (int q = 0; q < nt; ++q) {
+      const long long v = tot[q];
+      tot[q] = run;  // exclusive offsets
+      run += v;
+    }
+  }
+  __syncthreads();
+  long long run = tot[t];
+  for (long long i = lo; i < hi; ++i) {
+    run += a[i];
+    a[i] = run;
+  }
+}
+
+// Corrected arc curve: arc / (2 i (L - i) / L), clamped to [0, 1], 1 within
+// `window` of either end (discovery.hpp:72-74).
+__global__ void k_cac(const long long* __restrict__ arcs, long long L, long long window,
+                      double* __restrict__ cac) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= L) return;
+  double v = 1.0;
+  if (i >= window && i < L - window) {
+    const double ideal = 2.0 * (double)i * (double)(L - i) / (double)L;
+    v = ideal > 0.0 ? (double)arcs[i] / ideal : 1.0;
+    v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+  }
+  cac[i] = v;
+}
+
+// Block-level arg-extreme of v (finite entries; ties -> smallest index) into
+// one packed key per block; sign = +1 for max, -1 for min. Keys are reduced by
+// a second launch of the same kernel over the per-block results.
+__device__ __forceinline__ bool better(double a, long long ia, double b, long long ib, int sign) {
+  if (ia < 0) return false;
+  if (ib < 0) return true;
+  if (a != b) return sign > 0 ? a > b : a < b;
+  return ia < ib;
+}
+
+__global__ void k_argext(const double* __restrict__ v, const long long* __restrict__ vi,
+                         long long n, int sign, double* __restrict__ out_v,
+                         long long* __restrict__ out_i) {
+  __shared__ double sv[32];
+  __shared__ long long si[32];
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  double bv = 0.0;
+  long long bi = -1;
+  if (i < n) {
+    const double x = v[i];
+    const long long xi = vi ? vi[i] : i;
+    if (isfinite(x) && xi >= 0) { bv = x; bi = xi; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (better(ov, oi, bv, bi, sign)) { bv = ov; bi = oi; }
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) { sv[w] = bv; si[w] = bi; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = blockDim.x >> 5;
+    bv = lane < nw ? sv[lane] : 0.0;
+    bi = lane < nw ? si[lane] : -1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (better(ov, oi, bv, bi, sign)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) { out_v[blockIdx.x] = bv; out_i[blockIdx.x] = bi; }
+  }
+}
+
+// Mask |i - c| <= zone with `fill` (+inf to exclude from minima, -inf / NaN-free
+// sentinel for maxima).
+__global__ void k_mask_zone(double* __restrict__ v, long long n, long long c, long long zone,
+                            double fill) {
+  const long long i = (c - zone > 0 ? c - zone : 0) + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n && i <= c + zone) v[i] = fill;
+}
+
 // ---- K5: key merge -------------------------------------------------------------
 __global__ void k_keys_min(long long* __restrict__ dst, const long long* __restrict__ src,
                            long long len) {
