@@ -39,13 +39,14 @@ constexpr int kW = 32 * kD;                // diagonals per band = per warp item
 #define MPGPU_H 32
 #endif
 constexpr int kH = MPGPU_H;                // rows per warp tile
-constexpr int kRing = kW + 2 * kH;         // column ring slots per warp (320)
+constexpr int kRing = ((kW + 2 * kH + kD - 1) / kD) * kD;  // column ring slots per warp (320)
 constexpr int kNB = kRing / kD;            // blocks per ring plane (40)
 constexpr int kPad = kW + 2 * kH + 64;     // zero padding after the last window
 constexpr int kSeedChunk = 128;            // seed dot-product chunk (samples)
 constexpr long long kKeyNone = 0x7fffffffffffffffLL;
 
 static_assert(kRing % kD == 0, "ring must be a multiple of D");
+static_assert(kH % kD == 0, "tiles hold whole blocks of kD row-steps");
 
 struct Series {
   const double* x;   // raw samples, length n
@@ -370,17 +371,17 @@ __device__ __noinline__ SlowOut slow_path(const SlowIn in, unsigned live, int rt
 
 // Any cell over its threshold: hc[d] >= t[d], as a shallow predicate tree
 // (the compiler otherwise chains kD dependent ISETP.OR).
-static_assert(kD == 8 || kD == 16, "kD must be 8 or 16");
+static_assert(kD >= 4 && kD <= 16, "kD out of range");
 __device__ __forceinline__ bool any_ge(const int (&hc)[kD], const int (&t)[kD]) {
   unsigned r;
-  if constexpr (kD == 16) {
+  if constexpr (kD != 8 && kD != 4) {
     bool a = false, b = false, c = false, d = false;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kD; q += 4) {
       a |= hc[q] >= t[q];
-      b |= hc[4 + q] >= t[4 + q];
-      c |= hc[8 + q] >= t[8 + q];
-      d |= hc[12 + q] >= t[12 + q];
+      if (q + 1 < kD) b |= hc[q + 1] >= t[q + 1];
+      if (q + 2 < kD) c |= hc[q + 2] >= t[q + 2];
+      if (q + 3 < kD) d |= hc[q + 3] >= t[q + 3];
     }
     r = (a | b) | (c | d);
   } else if constexpr (kD == 8) {
@@ -627,7 +628,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
 // touches the row take the slow path). Cells on kInitDiag spread diagonals of
 // each pass, evaluated by direct centred dot products; they are ordinary
 // cells of the join, so min-merging them changes nothing but the filter.
-constexpr int kInitDiag = 8;
+#ifndef MPGPU_INIT_DIAG
+#define MPGPU_INIT_DIAG 32
+#endif
+constexpr int kInitDiag = MPGPU_INIT_DIAG;
 
 __global__ void k_init_keys(const Pass PS, long long klo, long long khi, int m, long long imask) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
