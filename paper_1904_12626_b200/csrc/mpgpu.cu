@@ -408,7 +408,8 @@ mpgpu_status mpgpu_plan_prepare(mpgpu_plan* p) {
     const long long klo = p->self ? p->zone + 1 : (q == 0 ? 0 : 1);
     const long long khi = ps.C.L;
     if (khi <= klo) continue;
-    dim3 grid((unsigned)((ps.R.L + 255) / 256), kInitDiag);
+    const int n_init = (int)std::max<long long>(8, std::min<long long>(kInitDiag, 8192 / p->m));
+    dim3 grid((unsigned)((ps.R.L + 255) / 256), (unsigned)n_init);
     k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask);
     p->launches += 1;
   }

@@ -628,6 +628,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
 // touches the row take the slow path). Cells on kInitDiag spread diagonals of
 // each pass, evaluated by direct centred dot products; they are ordinary
 // cells of the join, so min-merging them changes nothing but the filter.
+// The launch picks the diagonal count (grid.y): up to kInitDiag, fewer for long
+// windows where each cell's direct dot product costs more.
 #ifndef MPGPU_INIT_DIAG
 #define MPGPU_INIT_DIAG 32
 #endif
@@ -640,8 +642,8 @@ __global__ void k_init_keys(const Pass PS, long long klo, long long khi, int m, 
   const Series& C = PS.C;
   const long long span = khi - klo;
   if (span <= 0 || i >= R.L) return;
-  // diagonal b: klo + b*span/kInitDiag (b = 0 is the first admissible diagonal)
-  const long long k = klo + (span * b) / kInitDiag;
+  // diagonal b: klo + b*span/nb (b = 0 is the first admissible diagonal)
+  const long long k = klo + (span * b) / (long long)gridDim.y;
   const long long j = i + k;
   if (j >= C.L) return;
   const double ii = R.inv[i], ij = C.inv[j];
