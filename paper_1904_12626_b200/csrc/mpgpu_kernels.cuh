@@ -32,6 +32,10 @@ constexpr int kD = MPGPU_D;                // diagonals per thread (register blo
 #define MPGPU_MINBLOCKS 2
 #endif
 constexpr int kMinBlocks = MPGPU_MINBLOCKS;  // CTAs per SM the register budget targets
+#ifndef MPGPU_BLOCK
+#define MPGPU_BLOCK 8
+#endif
+constexpr int kBlock = MPGPU_BLOCK;          // row-steps per branch-free block (divides kD)
 constexpr int kWarps = MPGPU_WARPS;          // warps per CTA (independent workers)
 constexpr int kThreads = kWarps * 32;      // 256
 constexpr int kW = 32 * kD;                // diagonals per band = per warp item (256)
@@ -47,6 +51,7 @@ constexpr long long kKeyNone = 0x7fffffffffffffffLL;
 
 static_assert(kRing % kD == 0, "ring must be a multiple of D");
 static_assert(kH % kD == 0, "tiles hold whole blocks of kD row-steps");
+static_assert(kD % kBlock == 0, "blocks tile the kD-step rotation");
 
 struct Series {
   const double* x;   // raw samples, length n
@@ -519,55 +524,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       int b0 = (int)((ts / kD + lane) % kNB);
       for (int u = 0; u < kH; u += kD) {
         const int b1 = b0 + 1 == kNB ? 0 : b0 + 1;
-        double covs[kD];
 #pragma unroll
-        for (int d = 0; d < kD; ++d) covs[d] = cov[d];
-        bool anyfire = false;
+        for (int s0 = 0; s0 < kD; s0 += kBlock) {
+          double covs[kD];
 #pragma unroll
-        for (int s = 0; s < kD; ++s) {
-          const int h = u + s;
-          const int sin = (s + kD - 1) % kD;  // slot of the entering column
-          {
-            const int a = sin * kNB + (s == 0 ? b0 : b1);
-            cU[sin] = S.colU[a];
-            const double2 ci = S.colI[a];
-            cinv[sin] = ci.x;
-            cthr[sin] = __double2hiint(ci.y);
-          }
-          const double2 ru = S.rowU[buf][h];
-          const double2 ri = S.rowI[buf][h];
-          const int rthr = __double2hiint(ri.y);
-          int hcs[kD], tmin[kD];
+          for (int d = 0; d < kD; ++d) covs[d] = cov[d];
+          bool anyfire = false;
 #pragma unroll
-          for (int d = 0; d < kD; ++d) {
-            const int sl = (s + d) % kD;
-            cov[d] = fma(ru.x, cU[sl].y, cov[d]);
-            cov[d] = fma(ru.y, cU[sl].x, cov[d]);
-            hcs[d] = __double2hiint(cov[d] * (ri.x * cinv[sl]));  // rinv*cinv off the cov chain
-            tmin[d] = min(rthr, cthr[sl]);
-          }
-          anyfire |= any_ge(hcs, tmin);
-        }
-#ifdef MPGPU_EXPERIMENT_FASTONLY
-        if (anyfire && cov[0] == 12345.0) {  // never: measures the fast blocks alone
-#else
-        if (__builtin_expect(__any_sync(0xffffffffu, anyfire), 0)) {
-#endif
-          // ---- replay the block with exact key updates -----------------------
-#pragma unroll
-          for (int d = 0; d < kD; ++d) cov[d] = covs[d];
-#pragma unroll
-          for (int q = 0; q < kD - 1; ++q) {  // block-start window: columns rho + lane*kD + q
-            const int a = q * kNB + b0;
-            cU[q] = S.colU[a];
-            const double2 ci = S.colI[a];
-            cinv[q] = ci.x;
-            cthr[q] = __double2hiint(ci.y);
-          }
-#pragma unroll
-          for (int s = 0; s < kD; ++s) {
+          for (int s = s0; s < s0 + kBlock; ++s) {
             const int h = u + s;
-            const int sin = (s + kD - 1) % kD;
+            const int sin = (s + kD - 1) % kD;  // slot of the entering column
             {
               const int a = sin * kNB + (s == 0 ? b0 : b1);
               cU[sin] = S.colU[a];
@@ -578,31 +544,73 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
             const double2 ru = S.rowU[buf][h];
             const double2 ri = S.rowI[buf][h];
             const int rthr = __double2hiint(ri.y);
-            SlowIn in;
             int hcs[kD], tmin[kD];
 #pragma unroll
             for (int d = 0; d < kD; ++d) {
               const int sl = (s + d) % kD;
               cov[d] = fma(ru.x, cU[sl].y, cov[d]);
               cov[d] = fma(ru.y, cU[sl].x, cov[d]);
-              in.c[d] = cov[d] * (ri.x * cinv[sl]);
-              hcs[d] = __double2hiint(in.c[d]);
+              hcs[d] = __double2hiint(cov[d] * (ri.x * cinv[sl]));  // rinv*cinv off the cov chain
               tmin[d] = min(rthr, cthr[sl]);
             }
-            const bool fire = any_ge(hcs, tmin);
-            if (__any_sync(0xffffffffu, fire && ri.x != 0.0)) {
-              unsigned live = 0;
-              if (ri.x != 0.0) {
+            anyfire |= any_ge(hcs, tmin);
+          }
+#ifdef MPGPU_EXPERIMENT_FASTONLY
+          if (anyfire && cov[0] == 12345.0) {  // never: measures the fast blocks alone
+#else
+          if (__builtin_expect(__any_sync(0xffffffffu, anyfire), 0)) {
+#endif
+            // ---- replay the block with exact key updates ---------------------
 #pragma unroll
-                for (int d = 0; d < kD; ++d) live |= (cinv[(s + d) % kD] != 0.0 ? 1u : 0u) << d;
+            for (int d = 0; d < kD; ++d) cov[d] = covs[d];
+#pragma unroll
+            for (int q = 0; q < kD - 1; ++q) {  // block-start window: columns rho0 + lane*kD + q
+              const int a = ((s0 + q) % kD) * kNB + (s0 + q >= kD ? b1 : b0);
+              cU[(s0 + q) % kD] = S.colU[a];
+              const double2 ci = S.colI[a];
+              cinv[(s0 + q) % kD] = ci.x;
+              cthr[(s0 + q) % kD] = __double2hiint(ci.y);
+            }
+#pragma unroll
+            for (int s = s0; s < s0 + kBlock; ++s) {
+              const int h = u + s;
+              const int sin = (s + kD - 1) % kD;
+              {
+                const int a = sin * kNB + (s == 0 ? b0 : b1);
+                cU[sin] = S.colU[a];
+                const double2 ci = S.colI[a];
+                cinv[sin] = ci.x;
+                cthr[sin] = __double2hiint(ci.y);
               }
+              const double2 ru = S.rowU[buf][h];
+              const double2 ri = S.rowI[buf][h];
+              const int rthr = __double2hiint(ri.y);
+              SlowIn in;
+              int hcs[kD], tmin[kD];
 #pragma unroll
-              for (int d = 0; d < kD; ++d) in.cthr[d] = cthr[(s + d) % kD];
-              const long long rho = ts + h;
-              const SlowOut o = slow_path(in, live, rthr, r0 + rho, rho + (long long)lane * kD, c0,
-                                          h, buf, imask, PS.keyR, PS.keyC, P.stats);
+              for (int d = 0; d < kD; ++d) {
+                const int sl = (s + d) % kD;
+                cov[d] = fma(ru.x, cU[sl].y, cov[d]);
+                cov[d] = fma(ru.y, cU[sl].x, cov[d]);
+                in.c[d] = cov[d] * (ri.x * cinv[sl]);
+                hcs[d] = __double2hiint(in.c[d]);
+                tmin[d] = min(rthr, cthr[sl]);
+              }
+              const bool fire = any_ge(hcs, tmin);
+              if (__any_sync(0xffffffffu, fire && ri.x != 0.0)) {
+                unsigned live = 0;
+                if (ri.x != 0.0) {
 #pragma unroll
-              for (int d = 0; d < kD; ++d) cthr[(s + d) % kD] = o.cthr[d];
+                  for (int d = 0; d < kD; ++d) live |= (cinv[(s + d) % kD] != 0.0 ? 1u : 0u) << d;
+                }
+#pragma unroll
+                for (int d = 0; d < kD; ++d) in.cthr[d] = cthr[(s + d) % kD];
+                const long long rho = ts + h;
+                const SlowOut o = slow_path(in, live, rthr, r0 + rho, rho + (long long)lane * kD, c0,
+                                            h, buf, imask, PS.keyR, PS.keyC, P.stats);
+#pragma unroll
+                for (int d = 0; d < kD; ++d) cthr[(s + d) % kD] = o.cthr[d];
+              }
             }
           }
         }
