@@ -153,3 +153,34 @@ def test_multi_context_join_matches_single(mp):
     a2 = mp.join(x, y, 64, 0, devices=[0, 0])
     for k in a1:
         assert np.array_equal(a1[k], a2[k]), k
+
+
+def test_ab_join_edge_shapes(mp, oracle_lib):
+    """AB-joins with a one-window side, a side shorter than a band, and equal lengths."""
+    g = np.random.default_rng(61)
+    cases = [(300, 40, 40), (40, 300, 40), (5000, 120, 64), (120, 5000, 64), (777, 777, 50), (64, 64, 64)]
+    for na, nb, w in cases:
+        a = np.cumsum(g.standard_normal(na))
+        b = np.cumsum(g.standard_normal(nb))
+        pa, pb = mp.stomp_ab(a, b, w)
+        ra = oracle_lib.brute_force_mp(a, b, w)
+        rb = oracle_lib.brute_force_mp(b, a, w)
+        assert close(pa.values, ra[0])[0] and close(pb.values, rb[0])[0], (na, nb, w)
+        assert not index_mismatches(pa.index, ra[1], np.arange(pa.size()), a, b, w), (na, nb, w)
+        assert not index_mismatches(pb.index, rb[1], np.arange(pb.size()), b, a, w), (na, nb, w)
+
+
+def test_scrimp_ab_unsupported_on_gpu_api(mp):
+    x = np.cumsum(np.random.default_rng(62).standard_normal(500))
+    with pytest.raises(mp.UnsupportedError):
+        mp.scrimp(x, 20, 0.5, ts_b=x)
+    import ctypes
+    args = mp._JoinArgs()
+    a = np.ascontiguousarray(x)
+    args.a = a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    args.n_a = a.size
+    args.b = args.a
+    args.n_b = a.size
+    args.window = 20
+    cov = ctypes.c_double()
+    assert mp.lib().mpgpu_scrimp(ctypes.byref(args), 10, 0, ctypes.byref(cov)) == mp.MPGPU_EUNSUPPORTED
