@@ -144,8 +144,22 @@ mpgpu_plan *mpgpu_plan_create(const double *d_a, int64_t n_a, const double *d_b,
                               int64_t window, int64_t zone, int32_t device, void *cuda_stream);
 void mpgpu_plan_destroy(mpgpu_plan *plan);
 
-/* Window statistics + flat-window index, and reset the packed keys. */
+/* Window statistics + flat-window index, reset the packed keys, and warm-start
+ * them: a few spread diagonals, then (m >= 32 and >= 1e9 cells) the coarse warm
+ * start -- a join on the PAA-downsampled series whose matches seed exact cells
+ * of the full join. Equivalent to prepare_shard(0, 1) + prepare_finish. */
 mpgpu_status mpgpu_plan_prepare(mpgpu_plan *plan);
+
+/* Two-phase prepare for one process per GPU: every rank calls prepare_shard
+ * with its shard (the coarse join is sharded like the join itself), min-reduces
+ * the coarse keys from mpgpu_plan_coarse_keys across ranks (e.g. NCCL
+ * ReduceOp.MIN; both NULL / 0 when the plan has no coarse phase), then calls
+ * prepare_finish. The keys after prepare_finish are bit-identical to a
+ * single-rank mpgpu_plan_prepare. */
+mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan *plan, int32_t shard, int32_t n_shards);
+mpgpu_status mpgpu_plan_coarse_keys(mpgpu_plan *plan, int64_t **d_row_keys, int64_t *row_len,
+                                    int64_t **d_col_keys, int64_t *col_len);
+mpgpu_status mpgpu_plan_prepare_finish(mpgpu_plan *plan);
 
 /* Evaluate shard `shard` of `n_shards` (equal-cell contiguous ranges of the
  * diagonal work items) into the plan's keys. Shards of one plan may run in

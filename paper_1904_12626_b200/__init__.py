@@ -91,6 +91,13 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_plan_destroy.restype = None
     L.mpgpu_plan_prepare.argtypes = [ctypes.c_void_p]
     L.mpgpu_plan_prepare.restype = ctypes.c_int
+    L.mpgpu_plan_prepare_shard.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
+    L.mpgpu_plan_prepare_shard.restype = ctypes.c_int
+    L.mpgpu_plan_prepare_finish.argtypes = [ctypes.c_void_p]
+    L.mpgpu_plan_prepare_finish.restype = ctypes.c_int
+    L.mpgpu_plan_coarse_keys.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), _ip,
+                                         ctypes.POINTER(ctypes.c_void_p), _ip]
+    L.mpgpu_plan_coarse_keys.restype = ctypes.c_int
     L.mpgpu_plan_run.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
     L.mpgpu_plan_run.restype = ctypes.c_int
     L.mpgpu_plan_shard_cells.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
@@ -425,7 +432,31 @@ class Plan:
     __del__ = close
 
     def prepare(self) -> None:
+        """Stats, key reset and warm start (including the coarse join) on this GPU."""
         _check(lib().mpgpu_plan_prepare(self._p))
+
+    def prepare_shard(self, shard: int, n_shards: int) -> None:
+        """Phase 1 of a sharded prepare: this rank's shard of the coarse join.
+        Min-reduce coarse_keys() across ranks, then call prepare_finish()."""
+        _check(lib().mpgpu_plan_prepare_shard(self._p, int(shard), int(n_shards)))
+
+    def prepare_finish(self) -> None:
+        _check(lib().mpgpu_plan_prepare_finish(self._p))
+
+    def coarse_keys(self):
+        """(row_keys, col_keys) of the pending coarse join as int64 CUDA tensors,
+        or None when the plan has no coarse phase."""
+        import torch
+        pr, pc = ctypes.c_void_p(), ctypes.c_void_p()
+        lr, lc = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().mpgpu_plan_coarse_keys(self._p, ctypes.byref(pr), ctypes.byref(lr),
+                                            ctypes.byref(pc), ctypes.byref(lc)))
+        if not pr.value:
+            return None
+        dev = torch.device("cuda", self.device)
+        r = torch.as_tensor(_CudaArray(pr.value, lr.value, "<i8", self), device=dev)
+        c = torch.as_tensor(_CudaArray(pc.value, lc.value, "<i8", self), device=dev)
+        return r, c
 
     def run(self, shard: int = 0, n_shards: int = 1) -> None:
         _check(lib().mpgpu_plan_run(self._p, int(shard), int(n_shards)))

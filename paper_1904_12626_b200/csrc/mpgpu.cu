@@ -116,6 +116,12 @@ struct mpgpu_plan {
   // this plan's k_join reads thresholds from and RED.MINs into them directly
   long long* ext_key0 = nullptr;
   long long* ext_key1 = nullptr;
+  // coarse warm start (K2b): a nested plan on the PAA-downsampled series
+  int coarse_f = 0;  // 0: off
+  bool coarse_pending = false;  // coarse join done, exploit not yet run
+  mpgpu_plan* coarse = nullptr;
+  double* xc_a = nullptr;
+  double* xc_b = nullptr;
 };
 
 namespace {
@@ -261,6 +267,72 @@ JoinParams make_params(const mpgpu_plan* p) {
   return P;
 }
 
+// PAA factor of the coarse warm start: coarse window m/f = 16 samples. Off for
+// short windows, for series too short to leave a coarse profile, and when
+// MPGPU_COARSE=0 (experiments).
+long long join_cells_of(const mpgpu_plan* p) { return p->prefix.empty() ? 0 : p->prefix.back(); }
+
+int coarse_factor(const mpgpu_plan* p) {
+  static const bool off = getenv("MPGPU_COARSE") && atoi(getenv("MPGPU_COARSE")) == 0;
+  if (off) return 0;
+  static const int div = getenv("MPGPU_COARSE_DIV") ? atoi(getenv("MPGPU_COARSE_DIV")) : 16;
+  static const double min_cells = getenv("MPGPU_COARSE_MIN") ? atof(getenv("MPGPU_COARSE_MIN")) : 1e9;
+  if ((double)join_cells_of(p) < min_cells) return 0;
+  const long long f = p->m / div;
+  if (f < 2) return 0;
+  const long long mc = p->m / f;
+  const long long nA = p->A.n / f, nB = p->self ? nA : p->B.n / f;
+  const long long zc = p->self ? (p->zone + f - 1) / f : 0;
+  if (nA - mc + 1 < zc + 2 || nB - mc + 1 < 2) return 0;
+  return (int)f;
+}
+
+// K2b, phase 1: PAA series and (this shard of) the coarse join.
+mpgpu_status coarse_begin(mpgpu_plan* p, int shard, int n_shards) {
+  const int f = p->coarse_f;
+  const long long mc = p->m / f;
+  const long long nA = p->A.n / f, nB = p->self ? nA : p->B.n / f;
+  if (!p->coarse) {
+    MPG_CUDA(cudaMalloc(&p->xc_a, sizeof(double) * nA));
+    if (!p->self) MPG_CUDA(cudaMalloc(&p->xc_b, sizeof(double) * nB));
+    const long long zc = p->self ? (p->zone + f - 1) / f : 0;
+    p->coarse = mpgpu_plan_create(p->xc_a, nA, p->self ? nullptr : p->xc_b, nB, mc, zc,
+                                  p->device, p->stream);
+    if (!p->coarse) return MPGPU_ECUDA;
+  }
+  k_paa<<<(unsigned)((nA + 255) / 256), 256, 0, p->stream>>>(p->A.x, nA, f, p->xc_a);
+  if (!p->self) k_paa<<<(unsigned)((nB + 255) / 256), 256, 0, p->stream>>>(p->B.x, nB, f, p->xc_b);
+  p->launches += p->self ? 1 : 2;
+  mpgpu_status st = mpgpu_plan_prepare(p->coarse);
+  if (st == MPGPU_OK) st = mpgpu_plan_run(p->coarse, shard, n_shards);
+  if (st != MPGPU_OK) return st;
+  p->launches += p->coarse->launches;
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+// K2b, phase 2: seed the fine keys around the (merged) coarse matches. Coarse
+// row keys (best column per coarse row) and column keys (best row per coarse
+// column) both seed pass 0 of the fine plan (rows of A, columns of B).
+mpgpu_status coarse_finish(mpgpu_plan* p) {
+  const int f = p->coarse_f;
+  const JoinParams P = make_params(p);
+  const mpgpu_plan* c = p->coarse;
+  const long long Lr = c->A.L, Lc = c->self ? c->A.L : c->B.L;
+  // fine diagonals searched around each coarse match: +-f/2 (the PAA alignment
+  // error is below f; wider spans cost seeds for little gain)
+  static const int span_env = getenv("MPGPU_COARSE_SPAN") ? atoi(getenv("MPGPU_COARSE_SPAN")) : 0;
+  const int dspan = span_env > 0 ? span_env : std::max(1, f / 2);
+  const int nd = 2 * dspan + 1;
+  k_coarse_exploit<<<(unsigned)((Lr * nd + 255) / 256), 256, 0, p->stream>>>(
+      P.pass[0], c->key0, Lr, c->imask, false, f, dspan, p->zone, p->self, (int)p->m, p->imask);
+  k_coarse_exploit<<<(unsigned)((Lc * nd + 255) / 256), 256, 0, p->stream>>>(
+      P.pass[0], c->key1, Lc, c->imask, true, f, dspan, p->zone, p->self, (int)p->m, p->imask);
+  p->launches += 2;
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
 std::once_flag g_attr_once;
 int g_ctas_per_sm = 0;
 
@@ -366,6 +438,7 @@ mpgpu_plan* mpgpu_plan_create(const double* d_a, int64_t n_a, const double* d_b,
   // attribute is per-device: set it here as well for multi-device processes
   cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
   p->n_ctas = sms * std::max(1, g_ctas_per_sm);
+  p->coarse_f = coarse_factor(p.get());
   return p.release();
 }
 
@@ -373,6 +446,9 @@ void mpgpu_plan_destroy(mpgpu_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
   cudaStreamSynchronize(p->stream);
+  if (p->coarse) mpgpu_plan_destroy(p->coarse);
+  cudaFree(p->xc_a);
+  cudaFree(p->xc_b);
   p->A.release();
   p->B.release();
   cudaFree(p->key0);
@@ -385,7 +461,33 @@ void mpgpu_plan_destroy(mpgpu_plan* p) {
 }
 
 mpgpu_status mpgpu_plan_prepare(mpgpu_plan* p) {
+  const mpgpu_status st = mpgpu_plan_prepare_shard(p, 0, 1);
+  return st != MPGPU_OK ? st : mpgpu_plan_prepare_finish(p);
+}
+
+mpgpu_status mpgpu_plan_coarse_keys(mpgpu_plan* p, int64_t** d_row_keys, int64_t* row_len,
+                                    int64_t** d_col_keys, int64_t* col_len) {
   if (!p) return fail(MPGPU_EPARAM, "null plan");
+  const bool on = p->coarse_pending && p->coarse;
+  if (d_row_keys) *d_row_keys = on ? (int64_t*)p->coarse->key0 : nullptr;
+  if (row_len) *row_len = on ? p->coarse->A.L : 0;
+  if (d_col_keys) *d_col_keys = on ? (int64_t*)p->coarse->key1 : nullptr;
+  if (col_len) *col_len = on ? (p->coarse->self ? p->coarse->A.L : p->coarse->B.L) : 0;
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_plan_prepare_finish(mpgpu_plan* p) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (!p->coarse_pending) return MPGPU_OK;
+  MPG_CUDA(cudaSetDevice(p->device));
+  p->coarse_pending = false;
+  return coarse_finish(p);
+}
+
+mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
+  p->coarse_pending = false;
   MPG_CUDA(cudaSetDevice(p->device));
   p->launches = 0;
   mpgpu_status st = launch_stats(p, p->A);
@@ -408,10 +510,23 @@ mpgpu_status mpgpu_plan_prepare(mpgpu_plan* p) {
     const long long klo = p->self ? p->zone + 1 : (q == 0 ? 0 : 1);
     const long long khi = ps.C.L;
     if (khi <= klo) continue;
-    const int n_init = (int)std::max<long long>(8, std::min<long long>(kInitDiag, 8192 / p->m));
-    dim3 grid((unsigned)((ps.R.L + 255) / 256), (unsigned)n_init);
-    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask);
+    // spread diagonals: a handful when the coarse warm start follows (it finds
+    // far better candidates), kInitDiag otherwise
+    static const int n_env = getenv("MPGPU_INIT_N") ? atoi(getenv("MPGPU_INIT_N")) : -1;
+    const int n_init = n_env >= 0 ? n_env : (p->coarse_f > 0 ? 8 : kInitDiag);
+    if (n_init <= 0) continue;
+    // rows per thread: long enough to amortise the m-term seed, short enough
+    // that the grid still fills the GPU (~4 resident threads-worth per SM slot)
+    const long long fill = 148LL * 2048 * 4;
+    const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * n_init / fill));
+    dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)n_init);
+    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask, seg);
     p->launches += 1;
+  }
+  if (npass > 0 && p->coarse_f > 0) {
+    const mpgpu_status cs = coarse_begin(p, shard, n_shards);
+    if (cs != MPGPU_OK) return cs;
+    p->coarse_pending = true;
   }
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;

@@ -643,27 +643,111 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
 #endif
 constexpr int kInitDiag = MPGPU_INIT_DIAG;
 
-__global__ void k_init_keys(const Pass PS, long long klo, long long khi, int m, long long imask) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+constexpr int kInitSeg = 32;  // max rows per thread: one direct seed, then the recurrence
+
+__global__ void k_init_keys(const Pass PS, long long klo, long long khi, int m, long long imask,
+                            int seg) {
+  const long long i0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * seg;
   const int b = blockIdx.y;
   const Series& R = PS.R;
   const Series& C = PS.C;
   const long long span = khi - klo;
-  if (span <= 0 || i >= R.L) return;
+  if (span <= 0 || i0 >= R.L) return;
   // diagonal b: klo + b*span/nb (b = 0 is the first admissible diagonal)
   const long long k = klo + (span * b) / (long long)gridDim.y;
-  const long long j = i + k;
-  if (j >= C.L) return;
-  const double ii = R.inv[i], ij = C.inv[j];
-  if (ii == 0.0 || ij == 0.0) return;
-  const double mi = R.mu[i], mj = C.mu[j];
-  const double* xi = R.x + i;
-  const double* xj = C.x + j;
-  double acc = 0.0;
-  for (int t = 0; t < m; ++t) acc = fma(xi[t] - mi, xj[t] - mj, acc);
-  const double c = acc * ii * ij;
-  red_min(&PS.keyR[i], mk_key(c, j, imask));
-  red_min(&PS.keyC[j], mk_key(c, i, imask));
+  const long long j0 = i0 + k;
+  if (j0 >= C.L) return;
+  // seed cov(i0, j0) by a direct centred dot product, then walk the diagonal
+  // with the join's recurrence (the keys only have to be values of real cells)
+  const double mi = R.mu[i0], mj = C.mu[j0];
+  const double* xi = R.x + i0;
+  const double* xj = C.x + j0;
+  double acc0 = 0.0, acc1 = 0.0;
+  int t = 0;
+  for (; t + 1 < m; t += 2) {
+    acc0 = fma(xi[t] - mi, xj[t] - mj, acc0);
+    acc1 = fma(xi[t + 1] - mi, xj[t + 1] - mj, acc1);
+  }
+  if (t < m) acc0 = fma(xi[t] - mi, xj[t] - mj, acc0);
+  double cov = acc0 + acc1;
+  const long long n = min((long long)seg, min(R.L - i0, C.L - j0));
+  for (long long s = 0; s < n; ++s) {
+    const long long i = i0 + s, j = j0 + s;
+    if (s > 0) {
+      const double2 ru = R.U[i], cu = C.U[j];
+      cov = fma(ru.x, cu.y, cov);
+      cov = fma(ru.y, cu.x, cov);
+    }
+    const double ii = R.inv[i], ij = C.inv[j];
+    if (ii == 0.0 || ij == 0.0) continue;
+    const double c = cov * (ii * ij);
+    red_min(&PS.keyR[i], mk_key(c, j, imask));
+    red_min(&PS.keyC[j], mk_key(c, i, imask));
+  }
+}
+
+// ---- K2b: coarse warm start -------------------------------------------------------
+// A join on the PAA-downsampled series (factor f, window m/f) finds, for almost
+// every window, a match close to its best; warm-starting the keys there keeps
+// the join's filter from firing on the rising correlation runs that precede
+// each row's and column's best (a fire costs a replayed block). The coarse keys
+// are read directly (index = key & mask); each coarse pair (I, J) seeds the fine
+// diagonals f(J - I) + delta, |delta| <= f, over rows f*I .. f*I + f - 1: one
+// direct centred dot product, then the join's recurrence. Like K2 these are
+// real cells of the join, so they change the filter, never the answer.
+__global__ void k_paa(const double* __restrict__ x, long long nc, int f, double* __restrict__ xc) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= nc) return;
+  double s = 0.0;
+  for (int q = 0; q < f; ++q) s += x[t * f + q];
+  xc[t] = s / f;
+}
+
+__global__ void k_coarse_exploit(const Pass PS, const long long* __restrict__ ckey, long long Lc,
+                                 long long cimask, bool key_is_col, int f, int span,
+                                 long long zone, bool self, int m, long long imask) {
+  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int nd = 2 * span + 1;
+  const long long I = g / nd;
+  if (I >= Lc) return;
+  const long long kc = ckey[I];
+  if (kc == kKeyNone) return;
+  const long long J = kc & cimask;
+  const long long Ir = key_is_col ? J : I, Jc = key_is_col ? I : J;
+  const long long i0 = Ir * f, j0 = Jc * f + (long long)(g % nd) - span;
+  const Series& R = PS.R;
+  const Series& C = PS.C;
+  long long q0 = j0 < 0 ? -j0 : 0;
+  if (self && j0 - i0 <= zone) return;  // the whole segment lies in the zone (or below it)
+  long long qn = f;
+  qn = min(qn, R.L - i0);
+  qn = min(qn, C.L - j0);
+  if (q0 >= qn) return;
+  const long long is = i0 + q0, js = j0 + q0;
+  const double mi = R.mu[is], mj = C.mu[js];
+  const double* xi = R.x + is;
+  const double* xj = C.x + js;
+  double acc0 = 0.0, acc1 = 0.0;
+  int t = 0;
+  for (; t + 1 < m; t += 2) {
+    acc0 = fma(xi[t] - mi, xj[t] - mj, acc0);
+    acc1 = fma(xi[t + 1] - mi, xj[t + 1] - mj, acc1);
+  }
+  if (t < m) acc0 = fma(xi[t] - mi, xj[t] - mj, acc0);
+  double cov = acc0 + acc1;
+  for (long long q = q0; q < qn; ++q) {
+    const long long i = i0 + q, j = j0 + q;
+    if (q > q0) {
+      const double2 ru = R.U[i], cu = C.U[j];
+      cov = fma(ru.x, cu.y, cov);
+      cov = fma(ru.y, cu.x, cov);
+    }
+    const double ii = R.inv[i], ij = C.inv[j];
+    if (ii == 0.0 || ij == 0.0) continue;
+    const double c = cov * (ii * ij);
+    red_min(&PS.keyR[i], mk_key(c, j, imask));
+    red_min(&PS.keyC[j], mk_key(c, i, imask));
+  }
 }
 
 // ---- K6: distance-profile batch (MASS, distance.hpp:26-33) --------------------

@@ -2,8 +2,9 @@
 
 Every rank holds the whole series, evaluates an equal-cell shard of the
 diagonal work items (mpgpu_plan_run(shard=rank, n_shards=world)), and the
-packed int64 keys are min-reduced across ranks — the only exchange the join
-has. Rank `root` then decodes the keys into the profile.
+packed int64 keys are min-reduced across ranks — the join's only exchange
+(SURVEY.md §8e), plus the same MIN over the small coarse-join keys inside the
+sharded prepare (the warm start). Rank `root` then decodes the keys into the profile.
 Shards never change the arithmetic of a cell, so the result is bit-identical
 for any world size.
 """
@@ -26,11 +27,26 @@ def merge_keys_(row_keys, col_keys, group=None, root: Optional[int] = None) -> N
             dist.reduce(t, dst=root, op=op, group=group)
 
 
+def sharded_prepare(plan, rank: int, world: int, group=None) -> None:
+    """Prepare `plan` on every rank with the coarse warm start sharded too: each
+    rank runs its shard of the coarse join, the coarse keys are all-reduced with
+    MIN (every rank needs them), then each rank seeds its keys from them. The
+    keys end up bit-identical to a single-rank prepare."""
+    if world == 1:
+        plan.prepare()
+        return
+    plan.prepare_shard(rank, world)
+    ck = plan.coarse_keys()
+    if ck is not None:
+        merge_keys_(ck[0], ck[1], group=group, root=None)
+    plan.prepare_finish()
+
+
 def sharded_join(plan, rank: int, world: int, group=None, root: int = 0):
     """Run one rank's shard of `plan` (a paper_1904_12626_b200.Plan) and merge.
 
     Returns the MatrixProfile device arrays on `root`, None elsewhere."""
-    plan.prepare()
+    sharded_prepare(plan, rank, world, group=group)
     plan.run(rank, world)
     if world > 1:
         rk, ck = plan.keys()

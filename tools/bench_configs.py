@@ -25,6 +25,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="C1,C2,C3,C4,C5")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--cpu-seconds", type=float, default=6.0)
+ap.add_argument("--no-cpu", action="store_true", help="GPU numbers only (quick A/B runs)")
 args = ap.parse_args()
 
 for name in args.configs.split(","):
@@ -48,12 +49,12 @@ for name in args.configs.split(","):
     for r in range(2):
         out = mp.join(cfg.a, cfg.b, cfg.window, cfg.zone, want_b=cfg.b is not None, timed=True)
         tt.append(out["total_ms"])
-    cpu, thr, desc = cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
+    cpu, thr, desc = (None, 0, "skipped") if args.no_cpu else cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
     line = {"config": name, "workload": cfg.description, "cells": cfg.cells(),
             "gpu_ms": ms, "gpu_cells_per_s": cfg.cells() / (ms * 1e-3),
             "e2e_ms": min(tt), "e2e_cells_per_s": cfg.cells() / (min(tt) * 1e-3),
             "cpu_cells_per_s": cpu, "cpu_threads": thr, "cpu_sample": desc,
-            "speedup_e2e_vs_cpu": cfg.cells() / (min(tt) * 1e-3) / cpu}
+            "speedup_e2e_vs_cpu": cfg.cells() / (min(tt) * 1e-3) / cpu if cpu else None}
     print(json.dumps(line), flush=True)
     plan.close()
     del a, b
