@@ -1,4 +1,7 @@
-"""Upper bound of any warm start: time k_join when the keys already hold the exact answer."""
+"""Upper bound of any warm start: time k_join when the keys already hold the exact answer.
+
+    python tools/perfect_keys_bound.py C1,C2,C3,C4
+"""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
