@@ -100,6 +100,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(mhz)}
 
 
+def cpu_model() -> str:
+    """Host CPU model string (the lscpu 'Model name'), for the cpu_baseline record."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_sample_rate(cfg, seconds_target=15.0, threads=None):
     """Oracle STOMP (restated reference, oracle/) on a bounded row sample.
 
@@ -148,7 +160,8 @@ def run_reference(args, cfg, rank, world):
         "ms_per_step": cfg.cells() / v * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, datasets.py)",
         "config": {"workload": cfg.description, "config": cfg.name, "cells_per_step": cfg.cells()},
-        "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "port", "sample": desc},
+        "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "port", "sample": desc,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -269,7 +282,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, thr, desc = cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
-        cpu = {"value": rate, "unit": "cells/s", "cores": thr, "kind": "port", "sample": desc}
+        cpu = {"value": rate, "unit": "cells/s", "cores": thr, "kind": "port", "sample": desc,
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         prof = os.path.join(ROOT, "profiles", "k_join_traffic.json")

@@ -182,6 +182,9 @@ void build_items(mpgpu_plan* p) {
   const long long seg_fill = cells / ((long long)kW * 2 * ref_workers);
   long long seg = std::max(seg_balance, std::min<long long>(8 * p->m, seg_fill));
   seg = std::min<long long>(std::max<long long>(16384, 8 * p->m), seg);
+  // at most ~1e8 items (2.4 GB of item records; the queue index is an int):
+  // only series beyond ~2^27 samples reach this
+  seg = std::max<long long>(seg, cells / ((long long)kW * 100000000LL) + 1);
   seg = std::max<long long>(kH, (seg / kH) * kH);
   p->seg_rows = seg;
 
