@@ -215,11 +215,15 @@ def _ptr(a: Optional[np.ndarray], typ):
 
 def join(a, b=None, window: int = 4, zone: int = 0, *, n_gpus: int = 1,
          devices: Optional[Sequence[int]] = None, want_b: bool = True,
-         progress: Optional[Callable[[float], None]] = None, timed: bool = False):
+         progress: Optional[Callable[[float], None]] = None, timed: bool = False,
+         out: Optional[dict] = None):
     """Raw host-buffer join through ``mpgpu_join`` (zone already resolved).
 
     Returns a dict with mp_a, pi_a (+ left_a, right_a for self-joins; mp_b,
-    pi_b for AB-joins) and, when ``timed``, kernel_ms / total_ms.
+    pi_b for AB-joins) and, when ``timed``, kernel_ms / total_ms. ``out`` may
+    supply some or all of those arrays (C-contiguous, right dtype and length),
+    e.g. views of pinned host memory so the device-to-host copies run at full
+    speed; missing ones are allocated.
     """
     A = _series(a, "series")
     B = _series(b, "series B") if b is not None else None
@@ -227,7 +231,17 @@ def join(a, b=None, window: int = 4, zone: int = 0, *, n_gpus: int = 1,
     if B is not None:
         _check_window(window, B.size, "series B")
     La = A.size - window + 1
-    out = {"mp_a": np.empty(La), "pi_a": np.empty(La, np.int64)}
+    given = dict(out or {})
+
+    def _buf(name, n, dtype):
+        v = given.get(name)
+        if v is None:
+            return np.empty(n, dtype)
+        if not (isinstance(v, np.ndarray) and v.dtype == dtype and v.shape == (n,)
+                and v.flags.c_contiguous and v.flags.writeable):
+            raise ParameterError(f"out[{name!r}] must be a writable contiguous {np.dtype(dtype)} array of length {n}")
+        return v
+    out = {"mp_a": _buf("mp_a", La, np.float64), "pi_a": _buf("pi_a", La, np.int64)}
     args = _JoinArgs()
     args.a = _ptr(A, _dp)
     args.n_a = A.size
@@ -244,14 +258,14 @@ def join(a, b=None, window: int = 4, zone: int = 0, *, n_gpus: int = 1,
     args.mp_a = _ptr(out["mp_a"], _dp)
     args.pi_a = _ptr(out["pi_a"], _ip)
     if B is None:
-        out["left_a"] = np.empty(La, np.int64)
-        out["right_a"] = np.empty(La, np.int64)
+        out["left_a"] = _buf("left_a", La, np.int64)
+        out["right_a"] = _buf("right_a", La, np.int64)
         args.left_a = _ptr(out["left_a"], _ip)
         args.right_a = _ptr(out["right_a"], _ip)
     elif want_b:
         Lb = B.size - window + 1
-        out["mp_b"] = np.empty(Lb)
-        out["pi_b"] = np.empty(Lb, np.int64)
+        out["mp_b"] = _buf("mp_b", Lb, np.float64)
+        out["pi_b"] = _buf("pi_b", Lb, np.int64)
         args.mp_b = _ptr(out["mp_b"], _dp)
         args.pi_b = _ptr(out["pi_b"], _ip)
     cb = None

@@ -45,10 +45,22 @@ for name in args.configs.split(","):
         if r:
             times.append(e0.elapsed_time(e1))
     ms = min(times)
+    # e2e from pinned host memory both ways (as bench.py's e2e)
+    pa = torch.from_numpy(cfg.a).pin_memory().numpy()
+    pb = torch.from_numpy(cfg.b).pin_memory().numpy() if cfg.b is not None else None
+    La = cfg.a.size - cfg.window + 1
+    names = [("mp_a", La, torch.float64), ("pi_a", La, torch.int64)]
+    if cfg.b is None:
+        names += [("left_a", La, torch.int64), ("right_a", La, torch.int64)]
+    else:
+        Lb = cfg.b.size - cfg.window + 1
+        names += [("mp_b", Lb, torch.float64), ("pi_b", Lb, torch.int64)]
+    host_out = {k: torch.empty(n, dtype=t, pin_memory=True).numpy() for k, n, t in names}
     tt = []
-    for r in range(2):
-        out = mp.join(cfg.a, cfg.b, cfg.window, cfg.zone, want_b=cfg.b is not None, timed=True)
-        tt.append(out["total_ms"])
+    for r in range(3):
+        out = mp.join(pa, pb, cfg.window, cfg.zone, want_b=cfg.b is not None, timed=True, out=host_out)
+        if r:
+            tt.append(out["total_ms"])
     cpu, thr, desc = (None, 0, "skipped") if args.no_cpu else cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
     line = {"config": name, "workload": cfg.description, "cells": cfg.cells(),
             "gpu_ms": ms, "gpu_cells_per_s": cfg.cells() / (ms * 1e-3),
