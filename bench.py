@@ -303,7 +303,7 @@ def main():
                        "l2": "flushed between steps (256 MB write)",
                        "parallelism": f"diagonal shards x{world}, NCCL MIN merge" if world > 1 else "1 GPU",
                        "tile": mp.lib().mpgpu_build_info().decode()},
-            "roofline": {"bound": "fp64", "kernel": "k_join",
+            "roofline": {"bound": "fp64", "kernel": "k_join", "kernel_note": "the fine join launch (plan.run), timed alone with CUDA events; the coarse warm-start join is a separate small k_join launch inside prepare, counted in value and ms_per_step",
                          "achieved": join_ops_per_s / 1e12, "peak": FP64_PEAK_MEASURED / 1e12,
                          "unit": "Tops/s (fp64 ops, SURVEY §8d: 6 per cell)",
                          "frac": join_ops_per_s / FP64_PEAK_MEASURED,
