@@ -584,8 +584,9 @@ mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
     long long cells = 0;
     for (auto& it : mine) { (void)it; }
     for (size_t q = (size_t)shard; q < p->items.size(); q += (size_t)n_shards) cells += p->item_cells[q];
-    fprintf(stderr, "[mpgpu stats] cells %lld warp_row_steps %.3e slow_entries %llu (%.4f%%) row_cand %llu col_cand %llu\n",
-            cells, cells / 256.0, h[0], 100.0 * h[0] / (cells / 256.0), h[1], h[2]);
+    fprintf(stderr, "[mpgpu stats] cells %lld warp_row_steps %.3e slow_entries %llu (%.4f%%) row_cand %llu col_cand %llu replayed_blocks %llu (%.4f%% of blocks)\n",
+            cells, cells / 256.0, h[0], 100.0 * h[0] / (cells / 256.0), h[1], h[2], h[3],
+            100.0 * h[3] / (cells / 256.0 / kD));
     cudaFree(d_stats);
   }
   return MPGPU_OK;

@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
           if (__builtin_expect(__any_sync(0xffffffffu, anyfire), 0)) {
 #endif
             // ---- replay the block with exact key updates ---------------------
+            if (P.stats && lane == 0) atomicAdd(&P.stats[3], 1ull);
 #pragma unroll
             for (int d = 0; d < kD; ++d) cov[d] = covs[d];
 #pragma unroll
