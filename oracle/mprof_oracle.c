@@ -474,6 +474,10 @@ int or_scrimp_diagonals(const double *a, int64_t n_a, int64_t w, const int64_t *
       const int64_t x = bi[(size_t)L * t + j];
       if (d < mp[j] || (d == mp[j] && x >= 0 && x < pi[j])) { mp[j] = d; pi[j] = x; }
     }
+  /* near-zero hits recomputed directly, as in or_stomp (exact repeats -> 0) */
+  for (int64_t j = 0; j < L; ++j)
+    if (pi[j] >= 0 && mp[j] < 1e-3)
+      mp[j] = direct_dist(ac + j, mu[j], sd[j], ac + pi[j], mu[pi[j]], sd[pi[j]], w);
   free(bv); free(bi); free(mu); free(sd); free(ac);
   return 0;
 }
@@ -535,6 +539,10 @@ int or_scrimp(const double *a, int64_t n_a, int64_t w, double ez_fraction, int64
       if (d < lv[j] || (d == lv[j] && left && i < left[j])) { lv[j] = d; if (left) left[j] = i; }
     }
   }
+  /* near-zero hits recomputed directly, as in or_stomp (exact repeats -> 0) */
+  for (int64_t j = 0; j < L; ++j)
+    if (pi[j] >= 0 && mp[j] < 1e-3)
+      mp[j] = direct_dist(ac + j, mu[j], sd[j], ac + pi[j], mu[pi[j]], sd[pi[j]], w);
   const int full = todo == nd;
   if (!full) {
     if (left) for (int64_t j = 0; j < L; ++j) left[j] = -1;

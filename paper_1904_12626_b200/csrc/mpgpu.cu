@@ -112,6 +112,8 @@ struct mpgpu_plan {
   std::vector<long long> bands;
   long long* d_bands = nullptr;
   bool subset = false;
+  long long* d_init_diags = nullptr;  // anytime warm start: diagonals inside the chosen bands
+  int n_init_diags = 0;
   // keys owned by another plan (possibly on a peer device, reached over NVLink):
   // this plan's k_join reads thresholds from and RED.MINs into them directly
   long long* ext_key0 = nullptr;
@@ -459,6 +461,7 @@ void mpgpu_plan_destroy(mpgpu_plan* p) {
   cudaFree(p->d_items);
   cudaFree(p->d_counter);
   cudaFree(p->d_bands);
+  cudaFree(p->d_init_diags);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -523,7 +526,19 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
     const long long fill = 148LL * 2048 * 4;
     const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * n_init / fill));
     dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)n_init);
-    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask, seg);
+    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask, seg, nullptr);
+    p->launches += 1;
+  }
+  if (p->subset && p->n_init_diags > 0) {
+    // anytime run: warm start on diagonals of the chosen bands only (they are
+    // cells of this run), so no row's first visit fires every warp
+    const Pass& ps = P.pass[0];
+    const int n_init = p->n_init_diags;
+    const long long fill = 148LL * 2048 * 4;
+    const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * n_init / fill));
+    dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)n_init);
+    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, p->zone + 1, ps.C.L, (int)p->m, p->imask, seg,
+                                              p->d_init_diags);
     p->launches += 1;
   }
   if (npass > 0 && p->coarse_f > 0) {
@@ -678,6 +693,24 @@ mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int
                              cudaMemcpyHostToDevice, p->stream));
     MPG_CUDA(cudaStreamSynchronize(p->stream));
   }
+  // warm-start diagonals: the middle diagonal of up to kInitDiag chosen bands,
+  // spread over the chosen list
+  std::vector<long long> wd;
+  const long long L = p->A.L;
+  const int nw = (int)std::min<size_t>(kInitDiag, kb.size());
+  for (int q = 0; q < nw; ++q) {
+    const long long k = std::min(kb[(size_t)q * kb.size() / nw] + kW / 2, L - 1);
+    if (k > p->zone && (wd.empty() || wd.back() != k)) wd.push_back(k);
+  }
+  cudaFree(p->d_init_diags);
+  p->d_init_diags = nullptr;
+  p->n_init_diags = 0;
+  if (!wd.empty()) {
+    MPG_CUDA(cudaMalloc(&p->d_init_diags, sizeof(long long) * wd.size()));
+    MPG_CUDA(cudaMemcpy(p->d_init_diags, wd.data(), sizeof(long long) * wd.size(),
+                        cudaMemcpyHostToDevice));
+    p->n_init_diags = (int)wd.size();
+  }
   p->bands.swap(kb);
   p->subset = true;
   return MPGPU_OK;
@@ -770,9 +803,14 @@ mpgpu_status mpgpu_fluss(const int64_t* d_index, int64_t L, int64_t window, int6
   MPG_CUDA(cudaMemsetAsync(d_arcs, 0, sizeof(long long) * L, st));
   k_arc_ends<<<(unsigned)((L + 255) / 256), 256, 0, st>>>((const long long*)d_index, L,
                                                          (long long*)d_arcs);
-  k_scan_inclusive<<<1, 1024, 0, st>>>((long long*)d_arcs, L);
-  if (d_cac)
-    k_cac<<<(unsigned)((L + 255) / 256), 256, 0, st>>>((const long long*)d_arcs, L, window, d_cac);
+  const long long nt = (L + kScanTile - 1) / kScanTile;
+  long long* sums = nullptr;
+  if (cudaMallocAsync(&sums, sizeof(long long) * nt, st) != cudaSuccess)
+    return fail(MPGPU_ENOMEM, "FLUSS scan scratch");
+  k_scan_tile_sums<<<(unsigned)nt, kScanThreads, 0, st>>>((const long long*)d_arcs, L, sums);
+  k_scan_sums<<<1, 1024, 0, st>>>(sums, nt);
+  k_scan_tile_apply<<<(unsigned)nt, kScanThreads, 0, st>>>((long long*)d_arcs, L, sums, window, d_cac);
+  cudaFreeAsync(sums, st);
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
 }

@@ -647,15 +647,16 @@ constexpr int kInitDiag = MPGPU_INIT_DIAG;
 constexpr int kInitSeg = 32;  // max rows per thread: one direct seed, then the recurrence
 
 __global__ void k_init_keys(const Pass PS, long long klo, long long khi, int m, long long imask,
-                            int seg) {
+                            int seg, const long long* __restrict__ diags) {
   const long long i0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * seg;
   const int b = blockIdx.y;
   const Series& R = PS.R;
   const Series& C = PS.C;
   const long long span = khi - klo;
   if (span <= 0 || i0 >= R.L) return;
-  // diagonal b: klo + b*span/nb (b = 0 is the first admissible diagonal)
-  const long long k = klo + (span * b) / (long long)gridDim.y;
+  // diagonal b: klo + b*span/nb (b = 0 is the first admissible diagonal), or
+  // the b-th entry of an explicit list (anytime runs: diagonals of chosen bands)
+  const long long k = diags ? diags[b] : klo + (span * b) / (long long)gridDim.y;
   const long long j0 = i0 + k;
   if (j0 >= C.L) return;
   // seed cov(i0, j0) by a direct centred dot product, then walk the diagonal
@@ -868,46 +869,122 @@ __global__ void k_arc_ends(const long long* __restrict__ index, long long L,
   atomicAdd((unsigned long long*)&diff[hi], (unsigned long long)-1LL);
 }
 
-// Inclusive prefix sum in one block (L up to a few 1e7): per-thread chunk sums,
-// a block scan of the chunk totals, then the chunk rewrite.
-__global__ void k_scan_inclusive(long long* __restrict__ a, long long L) {
+// Inclusive prefix sum of the arc-end differences, in three coalesced passes:
+// per-tile sums, a scan of the tile sums, then each tile rescanned with its
+// offset. The last pass also writes the corrected arc curve (CAC), so the arc
+// counts are read once. 32 B of traffic per window plus the arc-end atomics.
+constexpr int kScanThreads = 256;
+constexpr int kScanPer = 16;
+constexpr int kScanTile = kScanThreads * kScanPer;  // 4096 windows per block
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(const long long* __restrict__ a,
+                                                                 long long L,
+                                                                 long long* __restrict__ sums) {
+  __shared__ long long ws[kScanThreads / 32];
+  const long long base = (long long)blockIdx.x * kScanTile;
+  long long s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {
+    const long long i = base + q * kScanThreads + threadIdx.x;
+    if (i < L) s += a[i];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < kScanThreads / 32; ++w) t += ws[w];
+    sums[blockIdx.x] = t;
+  }
+}
+
+// Exclusive scan of the n tile sums in one block (n = L / 4096: 2048 at 2^23).
+__global__ void k_scan_sums(long long* __restrict__ sums, long long n) {
   __shared__ long long tot[1024];
   const int t = threadIdx.x, nt = blockDim.x;
-  const long long chunk = (L + nt - 1) / nt;
-  const long long lo = t * chunk, hi = lo + chunk < L ? lo + chunk : L;
+  const long long chunk = (n + nt - 1) / nt;
+  const long long lo = t * chunk, hi = lo + chunk < n ? lo + chunk : n;
   long long s = 0;
-  for (long long i = lo; i < hi; ++i) s += a[i];
+  for (long long i = lo; i < hi; ++i) s += sums[i];
   tot[t] = s;
   __syncthreads();
   if (t == 0) {
     long long run = 0;
     for (int q = 0; q < nt; ++q) {
       const long long v = tot[q];
-      tot[q] = run;  // exclusive offsets
+      tot[q] = run;
       run += v;
     }
   }
   __syncthreads();
   long long run = tot[t];
   for (long long i = lo; i < hi; ++i) {
-    run += a[i];
-    a[i] = run;
+    const long long v = sums[i];
+    sums[i] = run;
+    run += v;
   }
 }
 
 // Corrected arc curve: arc / (2 i (L - i) / L), clamped to [0, 1], 1 within
 // `window` of either end (discovery.hpp:72-74).
-__global__ void k_cac(const long long* __restrict__ arcs, long long L, long long window,
-                      double* __restrict__ cac) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= L) return;
+__device__ __forceinline__ double cac_of(long long arcs, long long i, long long L, long long window) {
   double v = 1.0;
   if (i >= window && i < L - window) {
     const double ideal = 2.0 * (double)i * (double)(L - i) / (double)L;
-    v = ideal > 0.0 ? (double)arcs[i] / ideal : 1.0;
+    v = ideal > 0.0 ? (double)arcs / ideal : 1.0;
     v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
   }
-  cac[i] = v;
+  return v;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_tile_apply(long long* __restrict__ a, long long L,
+                                                                  const long long* __restrict__ offs,
+                                                                  long long window,
+                                                                  double* __restrict__ cac) {
+  __shared__ long long tile[kScanTile];
+  __shared__ long long ws[kScanThreads / 32];
+  const long long base = (long long)blockIdx.x * kScanTile;
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {  // coalesced load
+    const int k = q * kScanThreads + threadIdx.x;
+    tile[k] = base + k < L ? a[base + k] : 0;
+  }
+  __syncthreads();
+  // each thread scans kScanPer consecutive entries (a small bank conflict per
+  // step; the pass is bandwidth-bound)
+  long long v[kScanPer];
+  long long s = 0;
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {
+    s += tile[threadIdx.x * kScanPer + q];
+    v[q] = s;
+  }
+  // exclusive scan of the thread totals across the block
+  long long x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) >= o) x += y;
+  }
+  if ((threadIdx.x & 31) == 31) ws[threadIdx.x >> 5] = x;
+  __syncthreads();
+  long long wpre = 0;
+  for (int w = 0; w < (threadIdx.x >> 5); ++w) wpre += ws[w];
+  const long long pre = offs[blockIdx.x] + wpre + (x - s);
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) tile[threadIdx.x * kScanPer + q] = v[q] + pre;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kScanPer; ++q) {  // coalesced store (+ the CAC)
+    const int k = q * kScanThreads + threadIdx.x;
+    const long long i = base + k;
+    if (i < L) {
+      const long long arcs = tile[k];
+      a[i] = arcs;
+      if (cac) cac[i] = cac_of(arcs, i, L, window);
+    }
+  }
 }
 
 // Block-level arg-extreme of v (finite entries; ties -> smallest index) into
@@ -1068,26 +1145,43 @@ __global__ void k_finalize_self_partial(const Series A, const long long* __restr
   const long long L = A.L;
   long long rk = key_right[i], lk = key_left[i];
   const bool fi = A.inv[i] == 0.0;
-  // right neighbours j = i + k, bands ascending -> j ascending
-  long long rflat = -1, rany = -1;
-  for (int q = 0; q < n_bands && rflat < 0; ++q) {
-    const long long lo = i + bands[q];
-    const long long hi = min(i + min(bands[q] + kW, khi), L);  // exclusive
-    if (lo >= hi) continue;
-    if (rany < 0) rany = lo;
-    const long long f = next_flat(A, lo);
-    if (f >= 0 && f < hi) rflat = f;
+  // Smallest flat window and smallest admissible neighbour inside the chosen
+  // bands, on either side. The 32 lanes split the bands (each lane's share is
+  // ascending, so a lane stops at its first hit) and the warp takes the minima.
+  // Without any flat window in the series there is nothing to search.
+  constexpr long long kNoIdx = 0x7fffffffffffffffLL;
+  long long rflat = kNoIdx, rany = kNoIdx, lflat = kNoIdx, lany = kNoIdx;
+  if (next_flat(A, 0) >= 0) {
+    // right neighbours j = i + k
+    for (int q = lane; q < n_bands; q += 32) {
+      const long long lo = i + bands[q];
+      const long long hi = min(i + min(bands[q] + kW, khi), L);  // exclusive
+      if (lo >= hi) continue;
+      rany = min(rany, lo);
+      const long long f = next_flat(A, lo);
+      if (f >= 0 && f < hi) { rflat = f; break; }
+    }
+    // left neighbours j = i - k (band q covers j in [lo, hi))
+    for (int q = n_bands - 1 - lane; q >= 0; q -= 32) {
+      const long long lo = max(0LL, i - (min(bands[q] + kW, khi) - 1));
+      const long long hi = i - bands[q] + 1;  // exclusive
+      if (lo >= hi) continue;
+      lany = min(lany, lo);
+      const long long f = next_flat(A, lo);
+      if (f >= 0 && f < hi) { lflat = f; break; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      rflat = min(rflat, __shfl_xor_sync(0xffffffffu, rflat, o));
+      rany = min(rany, __shfl_xor_sync(0xffffffffu, rany, o));
+      lflat = min(lflat, __shfl_xor_sync(0xffffffffu, lflat, o));
+      lany = min(lany, __shfl_xor_sync(0xffffffffu, lany, o));
+    }
   }
-  // left neighbours j = i - k, bands descending -> j ascending
-  long long lflat = -1, lany = -1;
-  for (int q = n_bands - 1; q >= 0 && lflat < 0; --q) {
-    const long long lo = max(0LL, i - (min(bands[q] + kW, khi) - 1));
-    const long long hi = i - bands[q] + 1;  // exclusive
-    if (lo >= hi) continue;
-    if (lany < 0) lany = lo;
-    const long long f = next_flat(A, lo);
-    if (f >= 0 && f < hi) lflat = f;
-  }
+  if (rflat == kNoIdx) rflat = -1;
+  if (rany == kNoIdx) rany = -1;
+  if (lflat == kNoIdx) lflat = -1;
+  if (lany == kNoIdx) lany = -1;
   if (fi) {
     rk = rflat >= 0 ? mk_key_score(0.0, rflat, imask)
                     : (rany >= 0 ? mk_key_score(0.5, rany, imask) : kKeyNone);

@@ -49,6 +49,13 @@ def test_anytime_with_flat_runs(mp, oracle_lib):
     x[7000:7300] = 1.5
     nd = x.size - 50 + 1 - mp.zone_size(50, 0.25) - 1
     _check_subset(mp, oracle_lib, x, 50, 0.25, nd // 4, 5)
+    # more chosen bands than lanes (the finalize splits the band search over the warp)
+    y = np.cumsum(g.standard_normal(40000))
+    y[5000:5400] = y[5000]
+    y[21000:21150] = -3.0
+    y[33000:33100] = y[33000]
+    nd = y.size - 32 + 1 - mp.zone_size(32, 0.5) - 1
+    _check_subset(mp, oracle_lib, y, 32, 0.5, nd // 2, 6)
 
 
 def test_anytime_monotone_and_full(mp):

@@ -47,3 +47,15 @@ def test_discords_match_oracle_and_find_planted(mp, oracle_lib):
     p = mp.stomp(x, None, 50, 0.5)
     many, trunc = mp.find_discord(p, 100)
     assert trunc and len(many) == len(oracle_lib.extract(p.values, 100, p.exclusion_zone, True, -np.inf))
+
+
+def test_fluss_scan_tiles_match_oracle(mp, oracle_lib):
+    """Arc counts across several 4096-window scan tiles (and ragged tails) equal
+    the oracle's sweep exactly; the CAC matches to the last bit."""
+    g = np.random.default_rng(44)
+    for L in (4095, 4096, 4097, 3 * 4096 + 17, (1 << 20) + 5):
+        pi = g.integers(-1, L, L).astype(np.int64)
+        arcs, cac = mp.fluss(pi, 64)
+        ref = oracle_lib.fluss_arc_count(pi)
+        assert np.array_equal(arcs, ref), L
+        assert np.array_equal(cac, oracle_lib.fluss_cac(ref, 64)), L
