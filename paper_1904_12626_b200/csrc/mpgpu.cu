@@ -765,12 +765,18 @@ mpgpu_status mpgpu_distance_profiles(const double* d_ts, int64_t n, int64_t wind
   MPG_CUDA(cudaMallocAsync(&inv, sizeof(double) * L, st));
   k_window_stats<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(d_ts, L, (int)window, mu, inv,
                                                               nullptr, nullptr);
+  double* qstat = nullptr;
+  MPG_CUDA(cudaMallocAsync(&qstat, sizeof(double) * 3 * n_queries, st));
+  k_query_stats<<<(unsigned)((n_queries + 127) / 128), 128, 0, st>>>(
+      d_ts, d_queries, (const long long*)d_query_pos, (int)n_queries, (int)window, qstat);
   dim3 grid((unsigned)((L + kMassTile - 1) / kMassTile), (unsigned)n_queries);
   k_mass<<<grid, kMassThreads, 0, st>>>(d_ts, n, mu, inv, L, (int)window, d_queries,
-                                        (const long long*)d_query_pos, zone < 0 ? -1 : zone, d_out);
+                                        (const long long*)d_query_pos, qstat,
+                                        zone < 0 ? -1 : zone, d_out);
   MPG_CUDA(cudaGetLastError());
   MPG_CUDA(cudaFreeAsync(mu, st));
   MPG_CUDA(cudaFreeAsync(inv, st));
+  MPG_CUDA(cudaFreeAsync(qstat, st));
   return MPGPU_OK;
 }
 

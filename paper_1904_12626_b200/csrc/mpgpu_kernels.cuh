@@ -765,60 +765,76 @@ constexpr int kMassThreads = 128;
 constexpr int kMassR = 8;
 constexpr int kMassTile = kMassThreads * kMassR;  // outputs per CTA (1024)
 constexpr int kMassChunk = 512;                   // query samples staged per pass
+static_assert(kMassChunk % kMassR == 0, "query chunks in whole register-window rotations");
+// padded staging index: one gap per kMassR doubles, so lane l reading element
+// kMassR*l + c hits bank pair 2*(9l + c') -- conflict-free 2-wavefront loads
+__device__ __forceinline__ int mass_pad(int x) { return x + x / kMassR; }
+constexpr int kMassSx = kMassTile + kMassChunk + kMassR;
+constexpr int kMassSxPad = kMassSx + kMassSx / kMassR + 1;
+
+// Per-query statistics, once per query: mean, inverse norm (0 when flat) and
+// the sum of the centred samples, with the same sequential two-pass as K1, so
+// a query equal to a window of the series gets bit-identical statistics
+// (exact 0 on self-matches).
+__global__ void k_query_stats(const double* __restrict__ x, const double* __restrict__ queries,
+                              const long long* __restrict__ qpos, int n_queries, int m,
+                              double* __restrict__ qstat) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n_queries) return;
+  const double* qx = queries ? queries + (long long)q * m : x + qpos[q];
+  double s = 0.0;
+  for (int t = 0; t < m; ++t) s += qx[t];
+  const double mean = s / (double)m;
+  double ss = 0.0, asum = 0.0;
+  for (int t = 0; t < m; ++t) {
+    const double d = qx[t] - mean;
+    ss = fma(d, d, ss);
+    asum += d;
+  }
+  const double sd = sqrt(ss / (double)m);
+  const double scale = fabs(mean) > 1.0 ? fabs(mean) : 1.0;
+  qstat[3 * q + 0] = mean;
+  qstat[3 * q + 1] = sd <= 1e-10 * scale ? 0.0 : 1.0 / sqrt(ss);
+  qstat[3 * q + 2] = asum;
+}
 
 __global__ void __launch_bounds__(kMassThreads) k_mass(
     const double* __restrict__ x, long long n, const double* __restrict__ mu,
     const double* __restrict__ inv, long long L, int m, const double* __restrict__ queries,
-    const long long* __restrict__ qpos, long long zone, double* __restrict__ out) {
+    const long long* __restrict__ qpos, const double* __restrict__ qstat, long long zone,
+    double* __restrict__ out) {
   __shared__ double sq[kMassChunk];
-  __shared__ double sx[kMassTile + kMassChunk];
-  __shared__ double qstat[2];
+  __shared__ double sx[kMassSxPad];
   const int q = blockIdx.y;
   const long long j0 = (long long)blockIdx.x * kMassTile;
   const int tid = threadIdx.x;
   const double* qx = queries ? queries + (long long)q * m : x + qpos[q];
-  // query mean and inverse norm: the same sequential two-pass as K1, so a query
-  // equal to a window of the series gets bit-identical statistics (exact 0)
-  if (tid == 0) {
-    double s = 0.0;
-    for (int t = 0; t < m; ++t) s += qx[t];
-    const double mean = s / (double)m;
-    double ss = 0.0;
-    for (int t = 0; t < m; ++t) {
-      const double d = qx[t] - mean;
-      ss = fma(d, d, ss);
-    }
-    const double sd = sqrt(ss / (double)m);
-    const double scale = fabs(mean) > 1.0 ? fabs(mean) : 1.0;
-    qstat[0] = mean;
-    qstat[1] = sd <= 1e-10 * scale ? 0.0 : 1.0 / sqrt(ss);
-  }
-  __syncthreads();
-  const double qmean = qstat[0], qinv = qstat[1];
+  const double qmean = qstat[3 * q + 0], qinv = qstat[3 * q + 1], asum = qstat[3 * q + 2];
   double acc[kMassR];
 #pragma unroll
   for (int r = 0; r < kMassR; ++r) acc[r] = 0.0;
-  double asum = 0.0;
   const int jl = tid * kMassR;  // first local output of this thread
   for (int t0 = 0; t0 < m; t0 += kMassChunk) {
     const int tc = min(kMassChunk, m - t0);
-    for (int t = tid; t < tc; t += kMassThreads) sq[t] = qx[t0 + t] - qmean;
-    for (int t = tid; t < kMassTile + tc; t += kMassThreads) {
+    const int tcp = (tc + kMassR - 1) / kMassR * kMassR;  // zero-padded query tail
+    for (int t = tid; t < tcp; t += kMassThreads) sq[t] = t < tc ? qx[t0 + t] - qmean : 0.0;
+    for (int t = tid; t < kMassTile + tcp; t += kMassThreads) {
       const long long g = j0 + t0 + t;
-      sx[t] = g < n ? x[g] : 0.0;
+      sx[mass_pad(t)] = g < n ? x[g] : 0.0;
     }
     __syncthreads();
+    // rotating register window: slot (t + r) % kMassR holds x[jl + t + r]
     double w[kMassR];
 #pragma unroll
-    for (int r = 0; r < kMassR; ++r) w[r] = sx[jl + r];
-    for (int t = 0; t < tc; ++t) {
-      const double a = sq[t];
-      asum += a;
+    for (int r = 0; r < kMassR; ++r) w[r] = sx[mass_pad(jl + r)];
+    for (int t8 = 0; t8 < tcp; t8 += kMassR) {
 #pragma unroll
-      for (int r = 0; r < kMassR; ++r) acc[r] = fma(a, w[r], acc[r]);
+      for (int s = 0; s < kMassR; ++s) {
+        const double a = sq[t8 + s];
 #pragma unroll
-      for (int r = 0; r < kMassR - 1; ++r) w[r] = w[r + 1];
-      w[kMassR - 1] = sx[jl + kMassR + t];
+        for (int r = 0; r < kMassR; ++r) acc[r] = fma(a, w[(s + r) % kMassR], acc[r]);
+        w[s] = sx[mass_pad(jl + kMassR + t8 + s)];  // x[jl + t + 8] replaces x[jl + t]
+      }
     }
     __syncthreads();
   }
