@@ -520,12 +520,14 @@ class Plan:
         return o
 
 
-def distance_profiles(ts, window: int, queries=None, positions=None, zone: int = -1, stream=None):
+def distance_profiles(ts, window: int, queries=None, positions=None, zone: int = -1, stream=None,
+                      out=None):
     """MASS distance-profile batch on the GPU (mass_distance_profile, distance.hpp:26-33).
 
     ts: float64 CUDA tensor. Either `queries` (Q x window float64 CUDA tensor,
     external windows) or `positions` (Q int64 CUDA tensor of window starts in
-    ts; |j - pos| <= zone -> +inf, zone < 0: none). Returns a Q x L tensor."""
+    ts; |j - pos| <= zone -> +inf, zone < 0: none). Returns a Q x L tensor,
+    written into `out` when given (contiguous float64, same device)."""
     import torch
     _check_window(window, ts.numel(), "series")
     L = ts.numel() - window + 1
@@ -534,7 +536,11 @@ def distance_profiles(ts, window: int, queries=None, positions=None, zone: int =
     Q = queries.shape[0] if queries is not None else positions.numel()
     if queries is not None and (queries.dim() != 2 or queries.shape[1] != window):
         raise ParameterError("queries must be Q x window")
-    out = torch.empty((Q, L), dtype=torch.float64, device=ts.device)
+    if out is None:
+        out = torch.empty((Q, L), dtype=torch.float64, device=ts.device)
+    elif (tuple(out.shape) != (Q, L) or out.dtype != torch.float64 or out.device != ts.device
+          or not out.is_contiguous()):
+        raise ParameterError(f"out must be a contiguous float64 ({Q}, {L}) tensor on {ts.device}")
     st = stream if stream is not None else torch.cuda.current_stream(ts.device)
     _check(lib().mpgpu_distance_profiles(
         _dev_ptr(ts), ts.numel(), int(window),
