@@ -113,6 +113,19 @@ __device__ __forceinline__ double thr_filter(long long key, long long imask) {
   return t >= 0.0 ? t : -0.0;
 }
 
+// Fast-path form of a threshold: its hi word lowered by 3 units. The fast pass
+// tests corr computed with a cinv whose low 32 bits are replaced by the column
+// threshold (see pack_col): a relative error below 2^-20, i.e. under 3 hi-word
+// units, which the lowering absorbs (never skips a cell the exact test would
+// take). INT_MIN (always fire) stays.
+__device__ __forceinline__ int lower_thr(int h) { return h == INT_MIN ? h : h - 3; }
+// Packed column value: high word of cinv, low word the lowered threshold. The
+// fast pass uses it both as the (perturbed) cinv operand and as the threshold,
+// which frees a register per column slot; the replay reads the exact cinv.
+__device__ __forceinline__ double pack_col(double inv, int thr_lowered) {
+  return __hiloint2double(__double2hiint(inv), thr_lowered);
+}
+
 // ---- K1: statistics ----------------------------------------------------------
 // One thread per window; two passes over the window (exact, no cumsums).
 __global__ void k_window_stats(const double* __restrict__ x, long long L, int m,
@@ -228,9 +241,9 @@ __device__ __forceinline__ bool is_flat_at(const Series& s, long long p) {
 // raised by the slow path.
 struct __align__(16) WarpSmem {
   double2 colU[kRing];      // {df, dg} of ring columns, blocked-transposed
-  double2 colI[kRing];      // {inv, thr_filter}; .y stages the raw key on fetch
+  double2 colI[kRing];      // {inv, pack_col(inv, lowered thr)}; .y stages the raw key on fetch
   double2 rowU[2][kH + 1];  // +1: harmless read one past the tile
-  double2 rowI[2][kH + 1];  // {inv, thr_filter}; .y stages the raw key on fetch
+  double2 rowI[2][kH + 1];  // {inv, lowered thr in the hi word}; .y stages the raw key on fetch
   int zero;                 // always 0; read volatile to pin slow-path math
 };
 struct __align__(16) JoinSmem {
@@ -272,7 +285,8 @@ __device__ __forceinline__ void fix_col(WarpSmem& S, const Pass& PS, long long c
   const int a = ring_addr(x);
   const double2 v = S.colI[a];
   const bool live = (c0 + x) < PS.C.L && v.x != 0.0;
-  S.colI[a].y = live ? thr_filter(__double_as_longlong(v.y), imask) : 2.0;
+  const double t = live ? thr_filter(__double_as_longlong(v.y), imask) : 2.0;
+  S.colI[a].y = pack_col(v.x, lower_thr(__double2hiint(t)));
 }
 __device__ __forceinline__ void fetch_row(WarpSmem& S, const Pass& PS, int buf, int h, long long i) {
   cp_async16(&S.rowU[buf][h], &PS.R.U[i]);
@@ -283,7 +297,8 @@ __device__ __forceinline__ void fix_row(WarpSmem& S, const Pass& PS, int buf, in
                                         long long imask) {
   const double2 v = S.rowI[buf][h];
   const bool live = i < PS.R.L && v.x != 0.0;
-  S.rowI[buf][h].y = live ? thr_filter(__double_as_longlong(v.y), imask) : 2.0;
+  const double t = live ? thr_filter(__double_as_longlong(v.y), imask) : 2.0;
+  S.rowI[buf][h].y = __hiloint2double(lower_thr(__double2hiint(t)), 0);
 }
 
 // Rare path, entered by the whole warp when any lane's cell passed a row or
@@ -341,13 +356,13 @@ __device__ __noinline__ SlowOut slow_path(const SlowIn in, unsigned live, int rt
     const long long x = x0 + d;
     const long long key = mk_key(c, i, imask);
     red_min(&keyC[c0 + x], key);
-    const double t = thr_filter(key, imask);
-    const int th = __double2hiint(t);
+    const int th = lower_thr(__double2hiint(thr_filter(key, imask)));
 #pragma unroll
     for (int q = 0; q < kD; ++q)
       if (q == d && th > out.cthr[q]) out.cthr[q] = th;
     const int a = ring_addr(x);
-    if (th > __double2hiint(S.colI[a].y)) S.colI[a].y = t;  // lanes of one warp: benign race
+    const double2 ci = S.colI[a];
+    if (th > __double2loint(ci.y)) S.colI[a].y = pack_col(ci.x, th);  // lanes of one warp: benign race
   }
   // row: the lane's best candidate (largest corr, then smallest column), then the warp's
   if (__any_sync(0xffffffffu, rmask != 0)) {
@@ -366,8 +381,8 @@ __device__ __noinline__ SlowOut slow_path(const SlowIn in, unsigned live, int rt
     }
     if ((threadIdx.x & 31) == 0 && rbest != kKeyNone) {
       red_min(&keyR[i], rbest);
-      const double t = thr_filter(rbest, imask);
-      if (__double2hiint(t) > __double2hiint(S.rowI[buf][h].y)) S.rowI[buf][h].y = t;
+      const int th = lower_thr(__double2hiint(thr_filter(rbest, imask)));
+      if (th > __double2hiint(S.rowI[buf][h].y)) S.rowI[buf][h].y = __hiloint2double(th, 0);
     }
   }
   __syncwarp();
@@ -495,15 +510,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
     __syncwarp();
 
     double2 cU[kD];
-    double cinv[kD];
-    int cthr[kD];
+    double cpk[kD];  // pack_col: perturbed cinv (hi word) + lowered threshold (lo word)
 #pragma unroll
     for (int d = 0; d < kD - 1; ++d) {  // prime slots 0..D-2 with columns lane*D + d
       const int a = d * kNB + lane;
       cU[d] = S.colU[a];
-      const double2 ci = S.colI[a];
-      cinv[d] = ci.x;
-      cthr[d] = __double2hiint(ci.y);
+      cpk[d] = S.colI[a].y;
     }
 
     for (int t = 0; t < nT; ++t) {
@@ -537,9 +549,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
             {
               const int a = sin * kNB + (s == 0 ? b0 : b1);
               cU[sin] = S.colU[a];
-              const double2 ci = S.colI[a];
-              cinv[sin] = ci.x;
-              cthr[sin] = __double2hiint(ci.y);
+              cpk[sin] = S.colI[a].y;
             }
             const double2 ru = S.rowU[buf][h];
             const double2 ri = S.rowI[buf][h];
@@ -550,8 +560,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
               const int sl = (s + d) % kD;
               cov[d] = fma(ru.x, cU[sl].y, cov[d]);
               cov[d] = fma(ru.y, cU[sl].x, cov[d]);
-              hcs[d] = __double2hiint(cov[d] * (ri.x * cinv[sl]));  // rinv*cinv off the cov chain
-              tmin[d] = min(rthr, cthr[sl]);
+              hcs[d] = __double2hiint(cov[d] * (ri.x * cpk[sl]));  // rinv*cinv off the cov chain
+              tmin[d] = min(rthr, __double2loint(cpk[sl]));
             }
             anyfire |= any_ge(hcs, tmin);
           }
@@ -561,7 +571,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
           if (__builtin_expect(__any_sync(0xffffffffu, anyfire), 0)) {
 #endif
             // ---- replay the block with exact key updates ---------------------
+            // (exact cinv from the ring; thresholds from the packed low words)
             if (P.stats && lane == 0) atomicAdd(&P.stats[3], 1ull);
+            double cinv[kD];
+            int cthr[kD];
 #pragma unroll
             for (int d = 0; d < kD; ++d) cov[d] = covs[d];
 #pragma unroll
@@ -570,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
               cU[(s0 + q) % kD] = S.colU[a];
               const double2 ci = S.colI[a];
               cinv[(s0 + q) % kD] = ci.x;
-              cthr[(s0 + q) % kD] = __double2hiint(ci.y);
+              cthr[(s0 + q) % kD] = __double2loint(ci.y);
             }
 #pragma unroll
             for (int s = s0; s < s0 + kBlock; ++s) {
@@ -581,7 +594,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
                 cU[sin] = S.colU[a];
                 const double2 ci = S.colI[a];
                 cinv[sin] = ci.x;
-                cthr[sin] = __double2hiint(ci.y);
+                cthr[sin] = __double2loint(ci.y);
               }
               const double2 ru = S.rowU[buf][h];
               const double2 ri = S.rowI[buf][h];
@@ -612,6 +625,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
 #pragma unroll
                 for (int d = 0; d < kD; ++d) cthr[(s + d) % kD] = o.cthr[d];
               }
+            }
+            // back to the fast pass: packed values of the carried slots (the
+            // slow path may have raised their thresholds in the ring)
+#pragma unroll
+            for (int q = 0; q < kD - 1; ++q) {
+              const int sq_ = (s0 + kBlock + q) % kD;
+              cpk[sq_] = S.colI[sq_ * kNB + (s0 + kBlock + q >= kD ? b1 : b0)].y;
             }
           }
         }
