@@ -541,7 +541,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
           double covs[kD];
 #pragma unroll
           for (int d = 0; d < kD; ++d) covs[d] = cov[d];
-          bool anyfire = false;
+          // Fire test: max_d hc[d] >= rthr (3-input integer max) or hc[d] >=
+          // cthr[d] for some d; four predicate accumulators merged at block end.
+          bool fa = false, fb = false, fc = false, fd = false;
 #pragma unroll
           for (int s = s0; s < s0 + kBlock; ++s) {
             const int h = u + s;
@@ -554,17 +556,29 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
             const double2 ru = S.rowU[buf][h];
             const double2 ri = S.rowI[buf][h];
             const int rthr = __double2hiint(ri.y);
-            int hcs[kD], tmin[kD];
+            int hcs[kD];
 #pragma unroll
             for (int d = 0; d < kD; ++d) {
               const int sl = (s + d) % kD;
               cov[d] = fma(ru.x, cU[sl].y, cov[d]);
               cov[d] = fma(ru.y, cU[sl].x, cov[d]);
               hcs[d] = __double2hiint(cov[d] * (ri.x * cpk[sl]));  // rinv*cinv off the cov chain
-              tmin[d] = min(rthr, __double2loint(cpk[sl]));
             }
-            anyfire |= any_ge(hcs, tmin);
+            static_assert(kD == 8, "fire test written for 8 diagonals per lane");
+            const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
+            const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
+            const int m3 = __vimax3_s32(hcs[6], hcs[7], m1);
+            fa |= max(m2, m3) >= rthr;
+            fb |= hcs[0] >= __double2loint(cpk[(s + 0) % kD]);
+            fc |= hcs[1] >= __double2loint(cpk[(s + 1) % kD]);
+            fd |= hcs[2] >= __double2loint(cpk[(s + 2) % kD]);
+            fa |= hcs[3] >= __double2loint(cpk[(s + 3) % kD]);
+            fb |= hcs[4] >= __double2loint(cpk[(s + 4) % kD]);
+            fc |= hcs[5] >= __double2loint(cpk[(s + 5) % kD]);
+            fd |= hcs[6] >= __double2loint(cpk[(s + 6) % kD]);
+            fa |= hcs[7] >= __double2loint(cpk[(s + 7) % kD]);
           }
+          const bool anyfire = (fa | fb) | (fc | fd);
 #ifdef MPGPU_EXPERIMENT_FASTONLY
           if (anyfire && cov[0] == 12345.0) {  // never: measures the fast blocks alone
 #else
