@@ -348,9 +348,11 @@ extern "C" {
 const char* mpgpu_last_error(void) { return g_err.c_str(); }
 
 const char* mpgpu_build_info(void) {
-  static char buf[160];
-  snprintf(buf, sizeof(buf), "mprof_b200 sm_100a fp64 D=%d warps=%d W=%d H=%d ring=%d smem=%zu",
-           kD, kWarps, kW, kH, kRing, sizeof(JoinSmem));
+  static char buf[192];
+  // resident CTAs per SM as the occupancy API reports it (0 before any plan)
+  snprintf(buf, sizeof(buf),
+           "mprof_b200 sm_100a fp64 D=%d warps=%d W=%d H=%d ring=%d smem=%zu ctas_per_sm=%d", kD,
+           kWarps, kW, kH, kRing, sizeof(JoinSmem), g_ctas_per_sm);
   return buf;
 }
 
