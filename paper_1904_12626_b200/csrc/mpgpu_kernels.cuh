@@ -564,19 +564,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
               cov[d] = fma(ru.y, cU[sl].x, cov[d]);
               hcs[d] = __double2hiint(cov[d] * (ri.x * cpk[sl]));  // rinv*cinv off the cov chain
             }
-            static_assert(kD == 8, "fire test written for 8 diagonals per lane");
-            const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
-            const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
-            const int m3 = __vimax3_s32(hcs[6], hcs[7], m1);
-            fa |= max(m2, m3) >= rthr;
-            fb |= hcs[0] >= __double2loint(cpk[(s + 0) % kD]);
-            fc |= hcs[1] >= __double2loint(cpk[(s + 1) % kD]);
-            fd |= hcs[2] >= __double2loint(cpk[(s + 2) % kD]);
-            fa |= hcs[3] >= __double2loint(cpk[(s + 3) % kD]);
-            fb |= hcs[4] >= __double2loint(cpk[(s + 4) % kD]);
-            fc |= hcs[5] >= __double2loint(cpk[(s + 5) % kD]);
-            fd |= hcs[6] >= __double2loint(cpk[(s + 6) % kD]);
-            fa |= hcs[7] >= __double2loint(cpk[(s + 7) % kD]);
+            static_assert(kD == 8 || kD == 4, "fire test written for 4 or 8 diagonals per lane");
+            int rmax;
+            if constexpr (kD == 8) {
+              const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
+              const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
+              const int m3 = __vimax3_s32(hcs[6], hcs[7], m1);
+              rmax = max(m2, m3);
+            } else {
+              rmax = max(__vimax3_s32(hcs[0], hcs[1], hcs[2]), hcs[3]);
+            }
+            fa |= rmax >= rthr;
+            bool* acc4[4] = {&fb, &fc, &fd, &fa};
+#pragma unroll
+            for (int d = 0; d < kD; ++d) *acc4[d & 3] |= hcs[d] >= __double2loint(cpk[(s + d) % kD]);
           }
           const bool anyfire = (fa | fb) | (fc | fd);
 #ifdef MPGPU_EXPERIMENT_FASTONLY
