@@ -46,7 +46,11 @@ typedef enum {
  * zone is the RESOLVED half-width (mpgpu_zone_size), forced to 0 for AB-joins
  * (SPEC.md:268). Outputs have length n_a - window + 1 (mp_b/pi_b: n_b - window
  * + 1) and may be NULL when not wanted; left/right are self-join only.
- * Excluded / undefined entries are +inf and -1. */
+ * Excluded / undefined entries are +inf and -1.
+ * Samples must be finite: the reference validates them in the TimeSeries ctor
+ * (types.cpp:9-17), which the C++ and Python layers above this ABI mirror; the
+ * ABI itself does not rescan its inputs (results for non-finite samples are
+ * unspecified). The same holds for the device-resident plan API below. */
 typedef struct {
   const double *a;
   int64_t n_a;
