@@ -544,9 +544,14 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
     p->launches += 1;
   }
   if (npass > 0 && p->coarse_f > 0) {
-    const mpgpu_status cs = coarse_begin(p, shard, n_shards);
-    if (cs != MPGPU_OK) return cs;
-    p->coarse_pending = true;
+    // the coarse phase only tightens the filter: if it cannot run (e.g. the
+    // nested plan's allocations fail), the join proceeds without it
+    if (coarse_begin(p, shard, n_shards) == MPGPU_OK) {
+      p->coarse_pending = true;
+    } else {
+      p->coarse_f = 0;
+      cudaGetLastError();  // clear a non-sticky error; a sticky one resurfaces below
+    }
   }
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
