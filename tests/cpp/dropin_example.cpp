@@ -2,7 +2,8 @@
 // reads a raw fp64 series, runs mprof::stomp (profile.hpp:80-83) or
 // mprof::scrimp (profile.hpp:85-89), writes values/index/left/right as raw
 // arrays. Used by tests/test_dropin_cpp.py to show the drop-in boundary.
-//   dropin_example <in.f64> <window> <ez> <out_prefix> [stomp|scrimp|ab <b.f64>]
+//   dropin_example <in.f64> <window> <ez> <out_prefix>
+//                  [stomp|scrimp|anytime <s_size> <seed>|ab <b.f64>]
 #include <cstdio>
 #include <cstdlib>
 #include <exception>
@@ -30,7 +31,8 @@ static void write_vec(const std::string &path, const std::vector<T> &v) {
 
 int main(int argc, char **argv) {
   if (argc < 5) {
-    std::fprintf(stderr, "usage: %s in.f64 window ez out_prefix [stomp|scrimp|ab b.f64]\n", argv[0]);
+    std::fprintf(stderr, "usage: %s in.f64 window ez out_prefix [stomp|scrimp|anytime s seed|ab b.f64]\n",
+                 argv[0]);
     return 1;
   }
   const std::string mode = argc > 5 ? argv[5] : "stomp";
@@ -43,6 +45,8 @@ int main(int argc, char **argv) {
     mprof::MatrixProfile mp;
     if (mode == "scrimp") {
       mp = mprof::scrimp(a, w, ez);
+    } else if (mode == "anytime") {  // SCRIMP with s_size (anytime, profile.hpp:87-89)
+      mp = mprof::scrimp(a, w, ez, std::atoll(argv[6]), std::strtoull(argv[7], nullptr, 10), progress);
     } else if (mode == "ab") {
       mprof::TimeSeries b(read_f64(argv[6]));
       mp = mprof::stomp(a, &b, w, ez, 1, progress);
@@ -54,9 +58,10 @@ int main(int argc, char **argv) {
     write_vec(out + ".pi", mp.index);
     write_vec(out + ".left", mp.left_index);
     write_vec(out + ".right", mp.right_index);
-    std::printf("{\"size\": %lld, \"zone\": %lld, \"mode\": \"%s\", \"join\": \"%s\", \"progress_calls\": %d}\n",
+    std::printf("{\"size\": %lld, \"zone\": %lld, \"mode\": \"%s\", \"join\": \"%s\", "
+                "\"progress_calls\": %d, \"coverage\": %.17g}\n",
                 (long long)mp.size(), (long long)mp.exclusion_zone, mprof::mode_name(mp.mode),
-                mp.join_kind == mprof::JoinKind::self ? "self" : "ab", progress_calls);
+                mp.join_kind == mprof::JoinKind::self ? "self" : "ab", progress_calls, mp.coverage);
   } catch (const mprof::UnsupportedError &e) {
     std::printf("{\"error\": \"UnsupportedError\", \"what\": \"%s\"}\n", e.what());
     return 3;

@@ -30,10 +30,10 @@ def exe(tmp_path_factory):
     return out
 
 
-def _run(exe, tmp_path, a, w, ez, mode="stomp", b=None):
+def _run(exe, tmp_path, a, w, ez, mode="stomp", b=None, extra=()):
     inp = tmp_path / "a.f64"
     a.astype(np.float64).tofile(inp)
-    args = [exe, str(inp), str(w), str(ez), str(tmp_path / "out"), mode]
+    args = [exe, str(inp), str(w), str(ez), str(tmp_path / "out"), mode, *map(str, extra)]
     if b is not None:
         bp = tmp_path / "b.f64"
         b.astype(np.float64).tofile(bp)
@@ -79,3 +79,25 @@ def test_cpp_errors_map_to_reference_exceptions(exe, tmp_path):
     assert rc == 2 and info["error"] == "ParameterError"
     rc, info, _ = _run(exe, tmp_path, x[:3], 4, 0.5)
     assert rc == 2 and "too short" in info["what"]
+    bad = x.copy()
+    bad[17] = np.nan
+    rc, info, _ = _run(exe, tmp_path, bad, 8, 0.5)
+    assert rc == 2 and "not finite" in info["what"]
+
+
+def test_cpp_scrimp_anytime(exe, tmp_path, oracle_lib):
+    """mprof::scrimp with s_size (profile.hpp:87-89): a seeded band subset, coverage < 1,
+    left/right empty, values equal the oracle's SCRIMP over exactly those diagonals."""
+    import paper_1904_12626_b200 as mp
+    x = np.cumsum(np.random.default_rng(12).standard_normal(20000))
+    w, ez, seed = 64, 0.5, 4
+    zone = mp.zone_size(w, ez)
+    L = x.size - w + 1
+    s_size = (L - zone - 1) // 5
+    rc, info, res = _run(exe, tmp_path, x, w, ez, "anytime", extra=(s_size, seed))
+    bands, cov = mp.scrimp_bands(x.size, w, zone, s_size, seed)
+    assert rc == 0 and info["mode"] == "scrimp" and abs(info["coverage"] - cov) < 1e-15 and cov < 1.0
+    assert res["left"].size == 0 and res["right"].size == 0
+    ref_mp, ref_pi = oracle_lib.scrimp_diagonals(x, w, mp.band_diagonals(bands, L, zone))
+    assert close(res["mp"], ref_mp)[0]
+    assert not index_mismatches(res["pi"], ref_pi, np.arange(L), x, x, w)
