@@ -137,6 +137,69 @@ int64_t mpgpu_extract(const double *d_values, int64_t n, int64_t k, int64_t zone
                       double stop_at, int64_t *out_index, double *out_value, int32_t device,
                       void *cuda_stream);
 
+/* ---- multivariate joins (profile.hpp:91-100) ------------------------------
+ * Multivariate series are dim-major host arrays: x[dim * n + t], all
+ * dimensions of equal length (MultiTimeSeries, types.hpp:43-53). */
+
+/* SiMPle (mprof::simple_join, profile.hpp:96-100): per cell
+ * the non-normalised Euclidean distance summed over all dims,
+ * sqrt(sum_d |a_d,j - b_d,i|^2), with rounding residue of an exact match
+ * (<= 1e-12 of the summed window energies) snapped to 0
+ * (raw_distance_from_terms, distance.hpp:54-57). b == NULL -> self-join with
+ * `zone` (left / right filled as stomp); AB -> zone ignored (0). mp_a / pi_a:
+ * length n_a - window + 1, indexes into B (AB) or A; mp_b / pi_b (AB only,
+ * may be NULL): B against A from the same pass. kernel_ms (may be NULL):
+ * device time of the statistics, diagonal kernel and finalize. */
+typedef struct {
+  const double *a;
+  int64_t n_a;
+  const double *b;
+  int64_t n_b;
+  int64_t dims;
+  int64_t window;
+  int64_t zone;
+  int32_t device;
+  double *mp_a;
+  int64_t *pi_a;
+  int64_t *left_a;
+  int64_t *right_a;
+  double *mp_b;
+  int64_t *pi_b;
+  double *kernel_ms;
+} mpgpu_simple_args;
+
+mpgpu_status mpgpu_simple_join(const mpgpu_simple_args *args);
+
+/* mSTOMP (mprof::mstomp, profile.hpp:91-94): self-join,
+ * k-dimensional z-normalised profiles for every k at once. Per cell the
+ * per-dimension distances are ranked ascending with the must dims forced to
+ * the front (ascending among themselves), excluded dims removed, ties by
+ * dimension index; row k holds the minimum over partners of the mean of the
+ * k+1 first. Outputs are dims x L row-major (L = n - window + 1): values,
+ * index, and dim_order[k][i] = the dimension filling slot k at the chosen
+ * partner (MultiMatrixProfile, profile.hpp:48-62); rows k >= the number of
+ * admissible dims repeat the last full selection with dim_order -1.
+ * EPARAM: overlapping / repeated / out-of-range must or exc dims, or every
+ * dim excluded. EUNSUPPORTED: more than 32 admissible dims. */
+typedef struct {
+  const double *x;
+  int64_t n;
+  int64_t dims;
+  int64_t window;
+  int64_t zone;
+  const int64_t *must_dims;
+  int64_t n_must;
+  const int64_t *exc_dims;
+  int64_t n_exc;
+  int32_t device;
+  double *mp;
+  int64_t *pi;
+  int64_t *dim_order;
+  double *kernel_ms;
+} mpgpu_mstomp_args;
+
+mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args *args);
+
 /* ---- device-resident plan (sharded execution) --------------------------- */
 
 typedef struct mpgpu_plan mpgpu_plan;

@@ -63,6 +63,30 @@ def _load():
         lib.or_apply_exclusion_zone.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
         lib.or_merge_min.restype = None
         lib.or_merge_min.argtypes = [_dp, _ip, _dp, ctypes.c_int64, ctypes.c_int64]
+        lib.or_raw_norms.restype = None
+        lib.or_raw_norms.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, _dp]
+        lib.or_raw_sq_term.restype = ctypes.c_double
+        lib.or_raw_sq_term.argtypes = [ctypes.c_double] * 3
+        lib.or_raw_distance_from_terms.restype = ctypes.c_double
+        lib.or_raw_distance_from_terms.argtypes = [ctypes.c_double] * 2
+        lib.or_raw_direct.restype = ctypes.c_double
+        lib.or_raw_direct.argtypes = [_dp, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64,
+                                      ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]
+        lib.or_raw_distance_profile.argtypes = [_dp, _dp, ctypes.c_int64, ctypes.c_int64,
+                                                ctypes.c_int64, _dp]
+        lib.or_simple_join.argtypes = [_dp, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int64, ctypes.c_double, ctypes.c_int, ctypes.c_int64,
+                                       ctypes.c_int64, _dp, _ip, _ip, _ip]
+        lib.or_simple_brute.argtypes = [_dp, ctypes.c_int64, _dp, ctypes.c_int64, ctypes.c_int64,
+                                        ctypes.c_int64, ctypes.c_double, _dp, _ip, ctypes.c_int]
+        lib.or_mstomp.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
+                                  _ip, ctypes.c_int64, _ip, ctypes.c_int64, ctypes.c_int,
+                                  ctypes.c_int64, ctypes.c_int64, _dp, _ip, _ip]
+        lib.or_mstomp_dim_order.restype = ctypes.c_int64
+        lib.or_mstomp_dim_order.argtypes = [ctypes.c_int64, _ip, ctypes.c_int64, _ip, ctypes.c_int64,
+                                            _ip, _ip]
+        lib.or_mstomp_select.restype = None
+        lib.or_mstomp_select.argtypes = [_dp, ctypes.c_int64, ctypes.c_int64, _ip, _ip, _dp]
         _lib = lib
     return _lib
 
@@ -280,3 +304,114 @@ def extract(values, k, zone, largest, stop_at):
         out.append((j, float(v[j])))
         v[max(0, j - zone):j + zone + 1] = np.inf if not largest else -np.inf
     return out
+
+
+# ---------------------------------------------------------------- multivariate
+# SiMPle / mSTOMP (profile.hpp:91-100). Multivariate series are (dims, n)
+# arrays, passed dim-major.
+
+def _mts(x):
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim == 1:
+        x = x[None, :]
+    return np.ascontiguousarray(x)
+
+
+RAW_SNAP = 1e-12  # OR_RAW_SNAP (mprof_oracle.h)
+
+
+def raw_distance_from_terms(dsq, scale) -> float:
+    return float(_load().or_raw_distance_from_terms(float(dsq), float(scale)))
+
+
+def raw_sq_term(sa, sb, qt) -> float:
+    return float(_load().or_raw_sq_term(float(sa), float(sb), float(qt)))
+
+
+def raw_distance_profile(query, mts):
+    """raw_distance_profile (distance.hpp:44-49): query (dims, w) vs every window."""
+    q, x = _mts(query), _mts(mts)
+    if q.shape[0] != x.shape[0]:
+        raise ValueError("dimension mismatch")
+    out = np.empty(x.shape[1] - q.shape[1] + 1)
+    if _load().or_raw_distance_profile(_d(q), _d(x), x.shape[1], x.shape[0], q.shape[1], _d(out)):
+        raise ValueError("window out of range")
+    return out
+
+
+def raw_direct(a, i, b, j, w) -> float:
+    a, b = _mts(a), _mts(b)
+    return float(_load().or_raw_direct(_d(a), a.shape[1], _d(b), b.shape[1], a.shape[0], w, i, j))
+
+
+def simple_join(a, b=None, w=4, ez=0.5, n_workers=1, row_begin=0, row_end=0):
+    """simple (profile.hpp:96-100). Returns (mp, pi, left, right); AB: left/right None."""
+    a = _mts(a)
+    bb = _mts(b) if b is not None else None
+    if bb is not None and bb.shape[0] != a.shape[0]:
+        raise ValueError("dimension mismatch")
+    La = a.shape[1] - w + 1
+    mp, pi, le, ri = _alloc(La, True)
+    rc = _load().or_simple_join(_d(a), a.shape[1], _d(bb), 0 if bb is None else bb.shape[1],
+                                a.shape[0], w, ez, int(n_workers), int(row_begin), int(row_end),
+                                _d(mp), _i(pi), _i(le), _i(ri))
+    if rc:
+        raise ValueError("invalid window / fraction")
+    if b is not None:
+        le = ri = None
+    return mp, pi, le, ri
+
+
+def simple_brute(a, b=None, w=4, ez=0.5, threads=None):
+    a = _mts(a)
+    bb = _mts(b) if b is not None else None
+    La = a.shape[1] - w + 1
+    mp, pi = np.empty(La), np.empty(La, np.int64)
+    if _load().or_simple_brute(_d(a), a.shape[1], _d(bb), 0 if bb is None else bb.shape[1],
+                               a.shape[0], w, ez, _d(mp), _i(pi), threads or default_threads()):
+        raise ValueError("invalid window")
+    return mp, pi
+
+
+def _dimlist(v):
+    return np.ascontiguousarray(list(v) if v is not None else [], dtype=np.int64)
+
+
+def mstomp(x, w, ez=0.5, must_dims=(), exc_dims=(), n_workers=1, row_begin=0, row_end=0):
+    """mstomp (profile.hpp:91-94). Returns (values, index, dim_order), each (dims, L)."""
+    x = _mts(x)
+    d, n = x.shape
+    L = n - w + 1
+    must, exc = _dimlist(must_dims), _dimlist(exc_dims)
+    mp = np.empty((d, L))
+    pi = np.empty((d, L), np.int64)
+    do = np.empty((d, L), np.int64)
+    rc = _load().or_mstomp(_d(x), n, d, w, ez, _i(must), must.size, _i(exc), exc.size,
+                           int(n_workers), int(row_begin), int(row_end), _d(mp), _i(pi), _i(do))
+    if rc == -2:
+        raise ValueError("invalid must / exc dimensions")
+    if rc:
+        raise ValueError("invalid window / fraction")
+    return mp, pi, do
+
+
+def mstomp_dim_order(dims, must_dims=(), exc_dims=()):
+    must, exc = _dimlist(must_dims), _dimlist(exc_dims)
+    order = np.empty(max(dims, 1), np.int64)
+    nm = ctypes.c_int64(0)
+    c = _load().or_mstomp_dim_order(dims, _i(must), must.size, _i(exc), exc.size, _i(order),
+                                    ctypes.byref(nm))
+    if c < 0:
+        raise ValueError("invalid must / exc dimensions")
+    return order[:c], int(nm.value)
+
+
+def mstomp_select(dist, n_must, order):
+    """Per-cell selection: (slot dims, prefix means) for admissible distances
+    given in `order` (positions into order)."""
+    dist = _f64(dist)
+    order = np.ascontiguousarray(order, dtype=np.int64)
+    slot = np.empty(dist.size, np.int64)
+    pk = np.empty(dist.size)
+    _load().or_mstomp_select(_d(dist), dist.size, int(n_must), _i(order), _i(slot), _d(pk))
+    return slot, pk

@@ -26,6 +26,7 @@ __all__ = [
     "stomp", "scrimp", "scrimp_bands", "band_diagonals", "stomp_ab", "join", "Plan",
     "distance_profiles", "mass_distance_profile", "find_discord", "fluss", "fluss_extract",
     "rolling_stats", "lib", "K_FULL_RUN", "MIN_WINDOW",
+    "MultiTimeSeries", "MultiMatrixProfile", "simple_join", "mstomp",
 ]
 
 K_FULL_RUN = (1 << 63) - 1   # kFullRun (profile.hpp:20-21)
@@ -58,6 +59,25 @@ class _JoinArgs(ctypes.Structure):
         ("mp_a", _dp), ("pi_a", _ip), ("left_a", _ip), ("right_a", _ip),
         ("mp_b", _dp), ("pi_b", _ip),
         ("progress", _PROGRESS), ("progress_ctx", ctypes.c_void_p),
+    ]
+
+
+class _SimpleArgs(ctypes.Structure):
+    _fields_ = [
+        ("a", _dp), ("n_a", ctypes.c_int64), ("b", _dp), ("n_b", ctypes.c_int64),
+        ("dims", ctypes.c_int64), ("window", ctypes.c_int64), ("zone", ctypes.c_int64),
+        ("device", ctypes.c_int32),
+        ("mp_a", _dp), ("pi_a", _ip), ("left_a", _ip), ("right_a", _ip),
+        ("mp_b", _dp), ("pi_b", _ip), ("kernel_ms", _dp),
+    ]
+
+
+class _MStompArgs(ctypes.Structure):
+    _fields_ = [
+        ("x", _dp), ("n", ctypes.c_int64), ("dims", ctypes.c_int64), ("window", ctypes.c_int64),
+        ("zone", ctypes.c_int64), ("must_dims", _ip), ("n_must", ctypes.c_int64),
+        ("exc_dims", _ip), ("n_exc", ctypes.c_int64), ("device", ctypes.c_int32),
+        ("mp", _dp), ("pi", _ip), ("dim_order", _ip), ("kernel_ms", _dp),
     ]
 
 
@@ -135,6 +155,10 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_plan_attach_keys.restype = ctypes.c_int
     L.mpgpu_plan_num_bands.argtypes = [ctypes.c_void_p]
     L.mpgpu_plan_num_bands.restype = ctypes.c_int64
+    L.mpgpu_simple_join.argtypes = [ctypes.POINTER(_SimpleArgs)]
+    L.mpgpu_simple_join.restype = ctypes.c_int
+    L.mpgpu_mstomp.argtypes = [ctypes.POINTER(_MStompArgs)]
+    L.mpgpu_mstomp.restype = ctypes.c_int
     _lib = L
     return L
 
@@ -628,3 +652,162 @@ def rolling_stats(ts, window: int, stream=None):
                                      _dev_ptr(sd), ts.device.index or 0,
                                      ctypes.c_void_p(st.cuda_stream)))
     return mu, sd
+
+
+# ----------------------------------------------------------------- multivariate
+class MultiTimeSeries:
+    """Mirror of mprof::MultiTimeSeries (types.hpp:43-53; ctor types.cpp:20-32):
+    d >= 1 dimensions of equal length, each a validated TimeSeries. Built from
+    a (d, n) array or a sequence of 1-D series; ``data`` is dim-major."""
+
+    def __init__(self, dims):
+        if isinstance(dims, MultiTimeSeries):
+            self.data = dims.data
+            return
+        if isinstance(dims, np.ndarray) and dims.ndim == 2:
+            rows = [dims[q] for q in range(dims.shape[0])]
+        elif isinstance(dims, np.ndarray) and dims.ndim == 1:
+            rows = [dims]
+        else:
+            rows = list(dims)
+        if not rows:
+            raise ParameterError("multivariate series needs at least one dimension")
+        rows = [_series(r, f"dimension {q}") for q, r in enumerate(rows)]
+        n = rows[0].size
+        for q, r in enumerate(rows[1:], 1):
+            if r.size != n:
+                raise ParameterError(f"dimension {q} has length {r.size}, expected {n}")
+        self.data = np.ascontiguousarray(np.stack(rows))
+
+    def dims(self) -> int:
+        return int(self.data.shape[0])
+
+    def size(self) -> int:
+        return int(self.data.shape[1])
+
+    def dim(self, k: int) -> np.ndarray:
+        return self.data[k]
+
+
+@dataclass
+class MultiMatrixProfile:
+    """Mirror of mprof::MultiMatrixProfile (profile.hpp:48-62): row k is the
+    best (k+1)-dimensional profile; dim_order[k][i] the dimension filling slot
+    k at the chosen partner (-1 for an exhausted selection)."""
+    values: np.ndarray
+    index: np.ndarray
+    dim_order: np.ndarray
+    window: int = 0
+    exclusion_zone: int = 0
+    must_dims: tuple = ()
+    exc_dims: tuple = ()
+    data_len: int = 0
+    data_dims: int = 0
+
+    def size(self) -> int:
+        return 0 if self.values.size == 0 else int(self.values.shape[1])
+
+
+def simple_join(mts_a, mts_b=None, window: int = 4, ez_fraction: float = 0.5,
+                progress: Optional[Callable[[float], None]] = None, *, device: int = 0,
+                want_b: bool = False, timed: bool = False):
+    """mprof::simple_join (profile.hpp:96-100): SiMPle on the B200.
+
+    Non-normalised Euclidean distance summed over all dimensions; mts_b None
+    -> self-join (exclusion zone, left / right filled), else AB-join (zone 0).
+    ``want_b`` also returns B's profile against A from the same pass (as a
+    second MatrixProfile); ``timed`` attaches ``kernel_ms``."""
+    A = MultiTimeSeries(mts_a)
+    B = MultiTimeSeries(mts_b) if mts_b is not None else None
+    if B is not None and B.dims() != A.dims():
+        raise ParameterError(f"dimension mismatch: {A.dims()} vs {B.dims()}")
+    _check_window(window, A.size(), "series")
+    if B is not None:
+        _check_window(window, B.size(), "series B")
+    zone = zone_size(window, ez_fraction) if B is None else 0
+    La = A.size() - window + 1
+    mp_a, pi_a = np.empty(La), np.empty(La, np.int64)
+    args = _SimpleArgs()
+    args.a = _ptr(A.data, _dp)
+    args.n_a = A.size()
+    args.b = _ptr(B.data, _dp) if B is not None else None
+    args.n_b = 0 if B is None else B.size()
+    args.dims = A.dims()
+    args.window = int(window)
+    args.zone = int(zone)
+    args.device = int(device)
+    args.mp_a = _ptr(mp_a, _dp)
+    args.pi_a = _ptr(pi_a, _ip)
+    left = right = mp_b = pi_b = None
+    if B is None:
+        left, right = np.empty(La, np.int64), np.empty(La, np.int64)
+        args.left_a, args.right_a = _ptr(left, _ip), _ptr(right, _ip)
+    elif want_b:
+        Lb = B.size() - window + 1
+        mp_b, pi_b = np.empty(Lb), np.empty(Lb, np.int64)
+        args.mp_b, args.pi_b = _ptr(mp_b, _dp), _ptr(pi_b, _ip)
+    kms = ctypes.c_double(0)
+    args.kernel_ms = ctypes.pointer(kms)
+    _check(lib().mpgpu_simple_join(ctypes.byref(args)))
+    if progress is not None:
+        progress(1.0)
+    prof = MatrixProfile(values=mp_a, index=pi_a, window=window, mode="simple",
+                         data_len=A.size(), data_dims=A.dims())
+    if B is None:
+        prof.left_index, prof.right_index = left, right
+        prof.exclusion_zone = zone
+    else:
+        prof.join_kind = "ab"
+        prof.data_len_b = B.size()
+    if timed:
+        prof.kernel_ms = kms.value
+    if want_b and B is not None:
+        pb = MatrixProfile(values=mp_b, index=pi_b, window=window, mode="simple", join_kind="ab",
+                           data_len=B.size(), data_len_b=A.size(), data_dims=A.dims())
+        return prof, pb
+    return prof
+
+
+def mstomp(mts, window: int = 4, ez_fraction: float = 0.5, must_dims: Sequence[int] = (),
+           exc_dims: Sequence[int] = (), n_workers: int = 1,
+           progress: Optional[Callable[[float], None]] = None, *, device: int = 0,
+           timed: bool = False) -> MultiMatrixProfile:
+    """mprof::mstomp (profile.hpp:91-94): k-dimensional profiles for every k,
+    self-join only. Errors: must / exc overlap, repeated or
+    out-of-range dims, or every dim excluded -> ParameterError."""
+    if n_workers < 1:
+        raise ParameterError("n_workers must be >= 1")
+    X = MultiTimeSeries(mts)
+    _check_window(window, X.size(), "series")
+    zone = zone_size(window, ez_fraction)
+    d, L = X.dims(), X.size() - window + 1
+    must = np.ascontiguousarray(list(must_dims), dtype=np.int64)
+    exc = np.ascontiguousarray(list(exc_dims), dtype=np.int64)
+    vals = np.empty((d, L))
+    idx = np.empty((d, L), np.int64)
+    dorder = np.empty((d, L), np.int64)
+    args = _MStompArgs()
+    args.x = _ptr(X.data, _dp)
+    args.n = X.size()
+    args.dims = d
+    args.window = int(window)
+    args.zone = int(zone)
+    args.must_dims = _ptr(must, _ip) if must.size else None
+    args.n_must = must.size
+    args.exc_dims = _ptr(exc, _ip) if exc.size else None
+    args.n_exc = exc.size
+    args.device = int(device)
+    args.mp = _ptr(vals, _dp)
+    args.pi = _ptr(idx, _ip)
+    args.dim_order = _ptr(dorder, _ip)
+    kms = ctypes.c_double(0)
+    args.kernel_ms = ctypes.pointer(kms)
+    _check(lib().mpgpu_mstomp(ctypes.byref(args)))
+    if progress is not None:
+        progress(1.0)
+    r = MultiMatrixProfile(values=vals, index=idx, dim_order=dorder, window=window,
+                           exclusion_zone=zone, must_dims=tuple(int(q) for q in must),
+                           exc_dims=tuple(int(q) for q in exc), data_len=X.size(), data_dims=d)
+    if timed:
+        r.kernel_ms = kms.value
+    return r

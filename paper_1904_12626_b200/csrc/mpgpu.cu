@@ -18,6 +18,7 @@
 
 #include "mprof_gpu.h"
 #include "mpgpu_kernels.cuh"
+#include "mpgpu_internal.h"
 
 using namespace mpgpu;
 
@@ -342,6 +343,23 @@ std::once_flag g_attr_once;
 int g_ctas_per_sm = 0;
 
 }  // namespace
+
+namespace mpgpu_internal {
+
+mpgpu_status set_error(mpgpu_status st, const std::string& msg) { return fail(st, msg); }
+
+long long stats_pad() { return kPad; }
+
+cudaError_t series_stats(const double* d_x, long long n, int m, double* mu, double* inv,
+                         double2* U, uint8_t* flat, cudaStream_t st) {
+  const long long L = n - m + 1;
+  const int bs = 256;
+  k_window_stats<<<(unsigned)((L + bs - 1) / bs), bs, 0, st>>>(d_x, L, m, mu, inv, nullptr, flat);
+  k_update_vectors<<<(unsigned)((L + kPad + bs - 1) / bs), bs, 0, st>>>(d_x, mu, L, m, U, inv);
+  return cudaGetLastError();
+}
+
+}  // namespace mpgpu_internal
 
 extern "C" {
 

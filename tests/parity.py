@@ -55,3 +55,87 @@ def index_mismatches(got_idx, ref_idx, rows, x, y, m, tol=REL):
         if abs(dg - dr) > tol * max(dr, 1e-3) + ABS:
             bad.append((int(r), int(gi), int(ri), dg, dr))
     return bad
+
+
+# ---------------------------------------------------------------- multivariate
+RAW_SNAP = 1e-12  # raw_distance_from_terms snap (oracle OR_RAW_SNAP)
+
+
+def raw_exact(a: np.ndarray, i: int, b: np.ndarray, j: int, m: int) -> float:
+    """Direct SiMPle distance: sqrt(sum_d |a_d,i - b_d,j|^2), snapped to 0
+    below 1e-12 of the summed window energies. a, b: (dims, n)."""
+    x = a[:, i:i + m]
+    y = b[:, j:j + m]
+    d2 = float(np.sum((x - y) ** 2))
+    sc = float(np.sum(x * x) + np.sum(y * y))
+    return 0.0 if d2 <= RAW_SNAP * sc else float(np.sqrt(d2))
+
+
+def raw_index_mismatches(got_idx, ref_idx, rows, a, b, m, tol=REL):
+    bad = []
+    for r, gi, ri in zip(rows, got_idx, ref_idx):
+        if gi == ri:
+            continue
+        if gi < 0 or ri < 0:
+            bad.append((int(r), int(gi), int(ri)))
+            continue
+        dg = raw_exact(a, int(r), b, int(gi), m)
+        dr = raw_exact(a, int(r), b, int(ri), m)
+        if abs(dg - dr) > tol * max(dr, 1e-3) + ABS:
+            bad.append((int(r), int(gi), int(ri), dg, dr))
+    return bad
+
+
+def mstomp_order(dims, must=(), exc=()):
+    must = sorted(must)  # ascending, as the oracle and the GPU order them
+    order = must + [d for d in range(dims) if d not in must and d not in set(exc)]
+    return order, len(must)
+
+
+def mstomp_cell(x, i, j, m, order, n_must):
+    """Exact selection at cell (i, j): (slot dims, prefix means) with the must
+    dims first, each class ascending by distance, ties by position (stable)."""
+    dist = np.array([exact_dist(x[d], i, x[d], j, m) for d in order])
+    pos = list(range(len(order)))
+    head = sorted(pos[:n_must], key=lambda q: (dist[q], q))
+    tail = sorted(pos[n_must:], key=lambda q: (dist[q], q))
+    sel = head + tail
+    pk = np.cumsum(dist[sel]) / np.arange(1, len(sel) + 1)
+    return [order[q] for q in sel], pk, dist[sel]
+
+
+def mstomp_mismatches(got, ref, x, m, must=(), exc=(), tol=REL):
+    """Compare (values, index, dim_order) triples row by row. Index and
+    dim_order differences are accepted at near-ties of the exact values."""
+    gv, gi, gd = got
+    rv, ri, rd = ref
+    order, nm = mstomp_order(x.shape[0], must, exc)
+    D = len(order)
+    bad = []
+    ok, rel = close(gv.ravel(), rv.ravel(), tol)
+    if not ok:
+        bad.append(("values", rel))
+    for k in range(gv.shape[0]):
+        kk = min(k, D - 1)
+        for c in np.flatnonzero((gi[k] != ri[k]) | (gd[k] != rd[k])):
+            g, r = int(gi[k, c]), int(ri[k, c])
+            if g < 0 or r < 0:
+                if g != r:
+                    bad.append((k, int(c), g, r))
+                continue
+            sg, pg, dg = mstomp_cell(x, int(c), g, m, order, nm)
+            if g != r:
+                _, pr, _ = mstomp_cell(x, int(c), r, m, order, nm)
+                if abs(pg[kk] - pr[kk]) > tol * max(pr[kk], 1e-3) + ABS:
+                    bad.append((k, int(c), g, r, pg[kk], pr[kk]))
+                continue
+            # same partner, different dim_order: only at a near-tie around slot kk
+            if k >= D:
+                bad.append((k, int(c), "dim_order", int(gd[k, c]), int(rd[k, c])))
+                continue
+            lo = kk - 1 if kk > 0 else kk
+            hi = kk + 1 if kk + 1 < D else kk
+            near = any(abs(dg[q] - dg[kk]) <= tol * max(dg[kk], 1e-3) + ABS for q in (lo, hi) if q != kk)
+            if not near:
+                bad.append((k, int(c), "dim_order", int(gd[k, c]), int(rd[k, c]), sg[kk]))
+    return bad

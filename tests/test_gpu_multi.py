@@ -1,0 +1,186 @@
+"""GPU parity for the multivariate joins (SiMPle, mSTOMP; profile.hpp:91-100)
+through the C ABI (mpgpu_simple_join / mpgpu_mstomp) against the CPU oracle.
+
+Bar as for the univariate join: values within 1e-6 relative (1e-6 absolute
+near 0), +inf / -1 exact, indexes (and mSTOMP dim_order) identical except at
+near-ties of the exactly recomputed values (tests/parity.py)."""
+import numpy as np
+import pytest
+
+from tests.parity import close, mstomp_mismatches, raw_index_mismatches
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1904_12626_b200 as mp
+    mp.lib()
+    return mp
+
+
+def _walk(g, d, n):
+    return np.cumsum(g.standard_normal((d, n)), axis=1)
+
+
+def _check_simple_self(mp, oracle, a, w, ez, label):
+    got = mp.simple_join(a, None, w, ez)
+    ref = oracle.simple_join(a, None, w, ez, n_workers=oracle.default_threads())
+    ok, rel = close(got.values, ref[0])
+    assert ok, f"{label}: values (max rel {rel:.3e})"
+    rows = np.arange(got.values.size)
+    for name, g, r in (("index", got.index, ref[1]), ("left", got.left_index, ref[2]),
+                       ("right", got.right_index, ref[3])):
+        bad = raw_index_mismatches(g, r, rows, a, a, w)
+        assert not bad, f"{label}: {name} {bad[:4]}"
+
+
+def test_simple_self_sweep(mp, oracle_lib):
+    g = np.random.default_rng(1904)
+    for t in range(24):
+        d = int(g.integers(1, 6))
+        n = int(g.integers(64, 900))
+        w = int(g.integers(4, max(5, n // 4)))
+        ez = (0.0, 0.25, 0.5)[t % 3]
+        _check_simple_self(mp, oracle_lib, _walk(g, d, n), w, ez, f"case {t} d={d} n={n} w={w}")
+
+
+def test_simple_ab_both_directions(mp, oracle_lib):
+    g = np.random.default_rng(7)
+    for d, na, nb, w in ((1, 700, 300, 32), (3, 256, 513, 16), (4, 96, 96, 8)):
+        a, b = _walk(g, d, na), _walk(g, d, nb)
+        pa, pb = mp.simple_join(a, b, w, want_b=True)
+        ra = oracle_lib.simple_join(a, b, w)
+        rb = oracle_lib.simple_join(b, a, w)
+        for got, ref, x, y in ((pa, ra, a, b), (pb, rb, b, a)):
+            ok, rel = close(got.values, ref[0])
+            assert ok, f"AB d={d}: values (max rel {rel:.3e})"
+            bad = raw_index_mismatches(got.index, ref[1], np.arange(got.values.size), x, y, w)
+            assert not bad, bad[:4]
+        assert pa.join_kind == "ab" and pa.left_index.size == 0
+
+
+def test_simple_ab_self_identity(mp):
+    """mts_b = mts_a, no zone -> values 0 and index[i] = i."""
+    a = np.random.default_rng(3).standard_normal((3, 2000))
+    p = mp.simple_join(a, a, 40)
+    assert np.all(p.values == 0.0)
+    assert np.array_equal(p.index, np.arange(p.values.size))
+
+
+def test_simple_planted_chroma(mp):
+    """d = 12, two copies of a 40-column pattern in noise, w = 20."""
+    hits = 0
+    for seed in range(10):
+        g = np.random.default_rng(seed)
+        x = g.uniform(0, 1, (12, 1500))
+        pat = g.uniform(0, 1, (12, 40))
+        s1, s2 = int(g.integers(0, 600)), int(g.integers(800, 1400))
+        x[:, s1:s1 + 40] = pat + g.normal(0, 0.01, pat.shape)
+        x[:, s2:s2 + 40] = pat + g.normal(0, 0.01, pat.shape)
+        p = mp.simple_join(x, None, 20, 0.5)
+        c = int(np.argmin(p.values))
+        j = int(p.index[c])
+        hits += (s1 <= c <= s1 + 20 and s2 <= j <= s2 + 20) or (s2 <= c <= s2 + 20 and s1 <= j <= s1 + 20)
+    assert hits >= 9
+
+
+def test_simple_flat_runs_and_shift(mp, oracle_lib):
+    g = np.random.default_rng(17)
+    a = _walk(g, 2, 1200) + 1e4          # large offset: cancellation in the raw QT form
+    a[0, 200:400] = 3.0
+    a[1, 600:700] = -2.0
+    _check_simple_self(mp, oracle_lib, a, 24, 0.5, "flat+offset")
+
+
+def test_simple_larger(mp, oracle_lib):
+    g = np.random.default_rng(23)
+    _check_simple_self(mp, oracle_lib, _walk(g, 3, 12000), 64, 0.5, "d=3 n=12000")
+
+
+def _check_mstomp(mp, oracle, x, w, ez=0.5, must=(), exc=(), label=""):
+    got = mp.mstomp(x, w, ez, must, exc)
+    ref = oracle.mstomp(x, w, ez, must, exc, n_workers=oracle.default_threads())
+    bad = mstomp_mismatches((got.values, got.index, got.dim_order), ref, x, w, must, exc)
+    assert not bad, f"{label}: {bad[:4]}"
+    return got
+
+
+def test_mstomp_sweep(mp, oracle_lib):
+    g = np.random.default_rng(2019)
+    for t in range(16):
+        d = int(g.integers(1, 7))
+        n = int(g.integers(64, 700))
+        w = int(g.integers(4, max(5, n // 4)))
+        ez = (0.0, 0.25, 0.5)[t % 3]
+        _check_mstomp(mp, oracle_lib, _walk(g, d, n), w, ez, label=f"case {t} d={d} n={n} w={w}")
+
+
+@pytest.mark.parametrize("must,exc", [((2,), ()), ((), (1,)), ((3, 0), (2,)), ((1,), (0, 4))])
+def test_mstomp_must_exc(mp, oracle_lib, must, exc):
+    g = np.random.default_rng(5 + len(must))
+    _check_mstomp(mp, oracle_lib, _walk(g, 5, 500), 24, 0.5, must, exc, label=f"{must}/{exc}")
+
+
+def test_mstomp_many_dims(mp, oracle_lib):
+    """d > 8 runs the capacity-12 / 16 kernels with padding slots."""
+    g = np.random.default_rng(41)
+    _check_mstomp(mp, oracle_lib, _walk(g, 10, 300), 16, label="d=10")
+    _check_mstomp(mp, oracle_lib, _walk(g, 14, 200), 12, exc=(3,), label="d=14")
+
+
+def test_mstomp_reductions(mp, oracle_lib):
+    g = np.random.default_rng(43)
+    x = _walk(g, 2, 3000)
+    w = 64
+    st = mp.stomp(x[0], None, w, 0.5)
+    one = mp.mstomp(x[:1], w, 0.5)
+    assert np.max(np.abs(one.values[0] - st.values)) < 1e-8
+    assert np.all(one.dim_order[0] == 0)
+    ex = mp.mstomp(x, w, 0.5, exc_dims=(1,))
+    assert np.max(np.abs(ex.values[0] - st.values)) < 1e-8
+    assert np.array_equal(ex.values[1], ex.values[0]) and np.all(ex.dim_order[1] == -1)
+    full = mp.mstomp(x, w, 0.5)
+    assert np.all(full.values[0] <= full.values[1] + 1e-12)
+
+
+def test_mstomp_flat_windows(mp, oracle_lib):
+    g = np.random.default_rng(47)
+    x = _walk(g, 3, 900)
+    x[0, 100:300] = 1.5
+    x[2, 500:800] = 0.0
+    _check_mstomp(mp, oracle_lib, x, 32, label="flat")
+
+
+def test_mstomp_planted_motif(mp):
+    from tests.test_oracle_multi import planted_multivariate
+    hits = 0
+    for seed in range(20):
+        x, s1, s2 = planted_multivariate(seed, n=3000, m=64)
+        r = mp.mstomp(x, 64, 0.5)
+        c = int(np.argmin(r.values[1]))
+        pair = {c, int(r.index[1, c])}
+        near = all(min(abs(q - s1), abs(q - s2)) <= 2 for q in pair)
+        hits += near and {int(r.dim_order[0, c]), int(r.dim_order[1, c])} == {0, 1}
+    assert hits >= 18
+
+
+def test_mstomp_larger(mp, oracle_lib):
+    g = np.random.default_rng(53)
+    _check_mstomp(mp, oracle_lib, _walk(g, 3, 6000), 128, label="d=3 n=6000")
+
+
+def test_multivariate_errors(mp):
+    x = np.random.default_rng(1).standard_normal((3, 64))
+    for must, exc in (((0,), (0,)), ((), (0, 1, 2)), ((3,), ()), ((0, 0), ()), ((), (-1,))):
+        with pytest.raises(mp.ParameterError):
+            mp.mstomp(x, 8, 0.5, must, exc)
+    with pytest.raises(mp.ParameterError):
+        mp.simple_join(x, x[:2], 8)                                # dimension mismatch
+    with pytest.raises(mp.ParameterError):
+        mp.simple_join(x, None, 65)                                # window > n
+    with pytest.raises(mp.ParameterError):
+        mp.MultiTimeSeries([x[0], x[1][:50]])                      # unequal lengths
