@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -82,16 +83,23 @@ __device__ __forceinline__ double sqrt_search(double s) {
 }
 
 // ---- SiMPle ------------------------------------------------------------------
+// Keys are the squared distance's bits | index. kNoKeyS (the largest finite
+// double's bits) marks "no candidate": every finite value beats it while the
+// +inf of padded columns does not. Padding entries of the key arrays hold
+// kPadKey (hi word INT_MIN), so padded columns never pass the filter.
+constexpr long long kNoKeyS = 0x7fefffffffffffffLL;
+constexpr long long kPadKey = (long long)0x8000000000000000ULL;
+constexpr int kSimplePad = 8 * 32 + 64;  // entries of zero / +inf padding after the last window
 
 struct RawSeries {
-  const double* xc;   // dims x n, centred per dim (shared shift with the partner series)
-  const double* nrm;  // L: sum over dims of the centred window energies
-  long long n, L;
+  const double* xc;   // dims x ns (stride), centred per dim (shared shift), zero padded
+  const double* nrm;  // L + pad: summed centred window energies, +inf in the padding
+  long long n, ns, L;
 };
 struct SimplePass {
   RawSeries R, C;
   long long klo, khi;  // diagonals [klo, khi): cells (i, i + k)
-  long long* keyR;
+  long long* keyR;     // + padding (kPadKey)
   long long* keyC;
 };
 struct SimpleParams {
@@ -102,7 +110,128 @@ struct SimpleParams {
   long long imask;
 };
 
-__global__ void __launch_bounds__(kMWarps * 32) k_simple(const SimpleParams P) {
+__device__ __forceinline__ int key_hi(const long long* k, long long i) {
+  return reinterpret_cast<const int*>(k)[2 * i + 1];
+}
+
+// KD consecutive diagonals per lane (a 32*KD-diagonal band per warp), DIMS
+// compile-time. Column data of the lane's KD columns live in a register shift
+// window (one column enters per row-step); row data are broadcast loads. Per
+// cell: 2 DIMS DFMA (QT recurrence), one DADD + one DFMA for the squared
+// distance, and an integer filter on its high word against the row threshold
+// (min of the lane's KD high words) and the column's cached threshold. A step
+// in which any lane passes the filter runs the exact key update (RED.MIN).
+template <int KD, int DIMS>
+__global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_t(const SimpleParams P) {
+  const long long wid = (long long)blockIdx.x * kMWarps + (threadIdx.x >> 5);
+  if (wid >= P.n_items) return;
+  const int lane = threadIdx.x & 31;
+  const MItem it = P.items[wid];
+  const SimplePass& S = P.pass[it.pass];
+  const double* __restrict__ xr = S.R.xc;
+  const double* __restrict__ xc = S.C.xc;
+  const long long nsR = S.R.ns, nsC = S.C.ns;
+  const int m = P.m;
+  const long long r0 = it.r0;
+  const long long c0 = r0 + it.kb + (long long)lane * KD;  // column of diagonal 0 at row r0
+  const long long imask = P.imask;
+
+  double qt[KD];
+#pragma unroll
+  for (int d = 0; d < KD; ++d) qt[d] = 0.0;
+#pragma unroll
+  for (int q = 0; q < DIMS; ++q) {
+    const double* a = xr + q * nsR + r0;
+    const double* c = xc + q * nsC + c0;
+    for (int t = 0; t < m; ++t) {
+      const double av = a[t];
+#pragma unroll
+      for (int d = 0; d < KD; ++d) qt[d] = fma(av, c[t + d], qt[d]);
+    }
+  }
+  double co[KD][DIMS], cn[KD][DIMS], cnr[KD];
+  int cth[KD];
+#pragma unroll
+  for (int d = 0; d < KD - 1; ++d) {
+    const long long j = c0 + d;
+#pragma unroll
+    for (int q = 0; q < DIMS; ++q) {
+      co[d][q] = j > 0 ? xc[q * nsC + j - 1] : 0.0;
+      cn[d][q] = xc[q * nsC + j + m - 1];
+    }
+    cnr[d] = S.C.nrm[j];
+    cth[d] = key_hi(S.keyC, j);
+  }
+  for (int u = 0; u < it.nrows; u += KD) {
+#pragma unroll
+    for (int s = 0; s < KD; ++s) {
+      const long long i = r0 + u + s;
+      const int sin = (s + KD - 1) % KD;
+      {
+        const long long jn = c0 + u + s + KD - 1;  // entering column
+#pragma unroll
+        for (int q = 0; q < DIMS; ++q) {
+          co[sin][q] = jn > 0 ? xc[q * nsC + jn - 1] : 0.0;
+          cn[sin][q] = xc[q * nsC + jn + m - 1];
+        }
+        cnr[sin] = S.C.nrm[jn];
+        cth[sin] = key_hi(S.keyC, jn);
+      }
+      const bool step = (u + s) != 0;  // the seed row takes no update
+      double ro[DIMS], rn[DIMS];
+#pragma unroll
+      for (int q = 0; q < DIMS; ++q) {
+        ro[q] = step ? xr[q * nsR + i - 1] : 0.0;
+        rn[q] = step ? xr[q * nsR + i + m - 1] : 0.0;
+      }
+      const double rnr = S.R.nrm[i];
+      const int rth = key_hi(S.keyR, i);
+      double v[KD];
+      bool fire = false;
+      int hmin = 0x7fffffff;
+#pragma unroll
+      for (int d = 0; d < KD; ++d) {
+        const int sl = (s + d) % KD;
+#pragma unroll
+        for (int q = 0; q < DIMS; ++q) {
+          qt[d] = fma(-ro[q], co[sl][q], qt[d]);
+          qt[d] = fma(rn[q], cn[sl][q], qt[d]);
+        }
+        v[d] = fma(-2.0, qt[d], rnr + cnr[sl]);
+        const int h = __double2hiint(v[d]);
+        hmin = min(hmin, h);
+        fire |= h <= cth[sl];
+      }
+      fire |= hmin <= rth;
+      if (__any_sync(0xffffffffu, fire)) {
+        long long best = kNoKeyS;
+        const bool row_ok = i < S.R.L;
+#pragma unroll
+        for (int d = 0; d < KD; ++d) {
+          const int sl = (s + d) % KD;
+          const long long j = c0 + u + s + d;
+          const double vv = fmax(v[d], 0.0);
+          const int h = __double2hiint(vv);
+          if (row_ok && j < S.C.L) {
+            if (h <= cth[sl]) {
+              red_min64(&S.keyC[j], pack_key(vv, i, imask));
+              cth[sl] = min(cth[sl], h);
+            }
+            if (h <= rth) {
+              const long long kr = pack_key(vv, j, imask);
+              best = kr < best ? kr : best;
+            }
+          }
+        }
+        best = warp_min64(best);
+        if (lane == 0 && best != kNoKeyS) red_min64(&S.keyR[i], best);
+      }
+    }
+  }
+}
+
+// Any dimension count: one diagonal per lane, column data read per step.
+__global__ void __launch_bounds__(kMWarps * 32, 2) k_simple(const SimpleParams P) {
   const long long wid = (long long)blockIdx.x * kMWarps + (threadIdx.x >> 5);
   if (wid >= P.n_items) return;
   const int lane = threadIdx.x & 31;
@@ -110,43 +239,33 @@ __global__ void __launch_bounds__(kMWarps * 32) k_simple(const SimpleParams P) {
   const SimplePass& S = P.pass[it.pass];
   const long long k = it.kb + lane;
   const long long r0 = it.r0;
-  long long rend = r0 + it.nrows;
-  rend = min(rend, min(S.R.L, S.C.L - k));
-  if (k >= S.khi || rend < r0) rend = r0;
   const int m = P.m, dims = P.dims;
-  const long long nR = S.R.n, nC = S.C.n;
-
-  // seed: QT(r0, r0 + k) by a direct dot product over all dims
+  const long long nsR = S.R.ns, nsC = S.C.ns;
   double qt = 0.0;
-  if (r0 < rend) {
-    for (int d = 0; d < dims; ++d) {
-      const double* xr = S.R.xc + d * nR + r0;
-      const double* xc = S.C.xc + d * nC + r0 + k;
-      for (int t = 0; t < m; ++t) qt = fma(xr[t], xc[t], qt);
-    }
+  for (int d = 0; d < dims; ++d) {
+    const double* xr = S.R.xc + d * nsR + r0;
+    const double* xc = S.C.xc + d * nsC + r0 + k;
+    for (int t = 0; t < m; ++t) qt = fma(xr[t], xc[t], qt);
   }
-  const long long rmax = __reduce_max_sync(0xffffffffu, (unsigned)(rend - r0)) + r0;
-  for (long long i = r0; i < rmax; ++i) {
-    const bool live = i < rend;
+  for (long long i = r0; i < r0 + it.nrows; ++i) {
     const long long j = i + k;
-    long long kr = kNoKey;
-    if (live) {
-      if (i > r0) {
-        for (int d = 0; d < dims; ++d) {
-          const double* xr = S.R.xc + d * nR;
-          const double* xc = S.C.xc + d * nC;
-          qt = fma(-xr[i - 1], xc[j - 1], qt);
-          qt = fma(xr[i + m - 1], xc[j + m - 1], qt);
-        }
+    if (i > r0) {
+      for (int d = 0; d < dims; ++d) {
+        const double* xr = S.R.xc + d * nsR;
+        const double* xc = S.C.xc + d * nsC;
+        qt = fma(-xr[i - 1], xc[j - 1], qt);
+        qt = fma(xr[i + m - 1], xc[j + m - 1], qt);
       }
-      const double e = S.R.nrm[i] + S.C.nrm[j];
-      double v = fma(-2.0, qt, e);
-      v = v <= kRawSnap * e ? 0.0 : v;  // also clamps negatives
-      kr = pack_key(v, j, P.imask);
-      const long long kc = pack_key(v, i, P.imask);
+    }
+    const double vv = fmax(fma(-2.0, qt, S.R.nrm[i] + S.C.nrm[j]), 0.0);
+    const bool ok = i < S.R.L && j < S.C.L;
+    long long kr = kNoKeyS;
+    if (ok) {
+      kr = pack_key(vv, j, P.imask);
+      const long long kc = pack_key(vv, i, P.imask);
       if (kc < S.keyC[j]) red_min64(&S.keyC[j], kc);
     }
-    const long long tr = S.keyR[min(i, S.R.L - 1)];
+    const long long tr = S.keyR[i];
     if (__any_sync(0xffffffffu, kr < tr)) {
       const long long b = warp_min64(kr);
       if (lane == 0 && b < tr) red_min64(&S.keyR[i], b);
@@ -187,17 +306,17 @@ __global__ void k_simple_finalize(const double* X, long long nx, long long LX, c
   const int lane = threadIdx.x & 31;
   if (i >= LX) return;
   const long long a = k0[i];
-  const long long b = k1 ? k1[i] : kNoKey;
+  const long long b = k1 ? k1[i] : kNoKeyS;
   const long long best = a < b ? a : b;
-  const long long bi = best == kNoKey ? -1 : (best & imask);
+  const long long bi = best == kNoKeyS ? -1 : (best & imask);
   double v = INFINITY;
   if (bi >= 0) v = warp_raw_exact(X, nx, i, Y, ny, bi, dims, m, lane);
   if (lane == 0) {
     if (mp) mp[i] = v;
     if (pi) pi[i] = bi;
     // self: k0 = right keys (partners j > i), k1 = left keys (partners j < i)
-    if (right) right[i] = a == kNoKey ? -1 : (a & imask);
-    if (left) left[i] = b == kNoKey ? -1 : (b & imask);
+    if (right) right[i] = a == kNoKeyS ? -1 : (a & imask);
+    if (left) left[i] = b == kNoKeyS ? -1 : (b & imask);
   }
 }
 
@@ -206,22 +325,33 @@ __global__ void k_fill(long long* k, long long len) {
   if (i < len) k[i] = kNoKey;
 }
 
-// per-dim centring by a shared shift (distances are shift-invariant) and the
-// summed centred window energies (two passes per window, exact)
-__global__ void k_center(const double* __restrict__ x, long long n, int dims,
-                         const double* __restrict__ shift, double* __restrict__ xc) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n * dims) return;
-  xc[t] = x[t] - shift[t / n];
+__global__ void k_fill_val(long long* k, long long len, long long total, long long v, long long pad) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < total) k[i] = i < len ? v : pad;
 }
 
-__global__ void k_raw_energy(const double* __restrict__ xc, long long n, long long L, int dims,
-                             int m, double* __restrict__ nrm) {
+// per-dim centring by a shared shift (distances are shift-invariant) into a
+// zero-padded layout of stride ns
+__global__ void k_center(const double* __restrict__ x, long long n, long long ns, int dims,
+                         const double* __restrict__ shift, double* __restrict__ xc) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ns * dims) return;
+  const long long d = t / ns, p = t % ns;
+  xc[t] = p < n ? x[d * n + p] - shift[d] : 0.0;
+}
+
+// summed centred window energies (+inf in the padding)
+__global__ void k_raw_energy(const double* __restrict__ xc, long long ns, long long L,
+                             long long Lp, int dims, int m, double* __restrict__ nrm) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= L) return;
+  if (i >= Lp) return;
+  if (i >= L) {
+    nrm[i] = INFINITY;
+    return;
+  }
   double s = 0.0;
   for (int d = 0; d < dims; ++d) {
-    const double* w = xc + d * n + i;
+    const double* w = xc + d * ns + i;
     for (int t = 0; t < m; ++t) s = fma(w[t], w[t], s);
   }
   nrm[i] = s;
@@ -230,13 +360,13 @@ __global__ void k_raw_energy(const double* __restrict__ xc, long long n, long lo
 // ---- mSTOMP --------------------------------------------------------------------
 
 struct MStompParams {
-  const double* x;    // D x n (admissible dims, must first)
-  const double* mu;   // D x L
+  const double* x;    // D x ns (admissible dims, must first; zero padded)
+  const double* mu;   // D x Lp (zero padded)
   const double* inv;  // D x Lp (0: flat / padding)
   const double2* U;   // D x Lp
-  long long n, L, Lp;
+  long long n, ns, L, Lp;
   long long khi;      // diagonals [klo, khi) = [zone + 1, L)
-  long long* keys;    // D x L
+  long long* keys;    // D x Lp: kNoKeyS when empty, kPadKey in the padding
   const MItem* items;
   long long n_items;
   int m, n_must;
@@ -277,9 +407,9 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mstomp(const MStompParams P) {
   for (int q = 0; q < D; ++q) {
     cov[q] = 0.0;
     if (r0 < rend && q < P.D) {
-      const double* xr = P.x + q * P.n + r0;
-      const double* xc = P.x + q * P.n + r0 + k;
-      const double mr = P.mu[q * P.L + r0], mc = P.mu[q * P.L + r0 + k];
+      const double* xr = P.x + q * P.ns + r0;
+      const double* xc = P.x + q * P.ns + r0 + k;
+      const double mr = P.mu[q * P.Lp + r0], mc = P.mu[q * P.Lp + r0 + k];
       double acc = 0.0, asum = 0.0;
       for (int t = 0; t < m; ++t) {
         const double a = xr[t] - mr;
@@ -321,7 +451,7 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mstomp(const MStompParams P) {
       if (q >= P.D) break;
       acc += __longlong_as_double((long long)(s[q] & ~kFree));
       const double pk = acc * (1.0 / (double)(q + 1));
-      long long* kq = P.keys + q * P.L;
+      long long* kq = P.keys + q * P.Lp;
       const long long kr = live ? pack_key(pk, j, P.imask) : kNoKey;
       if (live) {
         const long long kc = pack_key(pk, i, P.imask);
@@ -331,6 +461,139 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mstomp(const MStompParams P) {
       if (__any_sync(0xffffffffu, kr < tr)) {
         const long long b = warp_min64(kr);
         if (lane == 0 && b < tr) red_min64(&kq[i], b);
+      }
+    }
+  }
+}
+
+// KD consecutive diagonals per lane, D admissible dims compile-time. Column
+// statistics of the lane's KD columns ({df, dg}, inv and the D column
+// thresholds) live in a register shift window; row statistics are broadcast
+// loads. Per cell: D covariance recurrences (2 DFMA each), D distances, the
+// stable sort, D prefix means and an integer filter of their high words
+// against the row / column thresholds; a step where any lane passes runs the
+// exact key updates.
+template <int KD, int D>
+__global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams P) {
+  const long long wid = (long long)blockIdx.x * kMWarps + (threadIdx.x >> 5);
+  if (wid >= P.n_items) return;
+  const int lane = threadIdx.x & 31;
+  const MItem it = P.items[wid];
+  const long long r0 = it.r0;
+  const long long c0 = r0 + it.kb + (long long)lane * KD;
+  const long long Lp = P.Lp, L = P.L;
+  const int m = P.m;
+  const double two_m = 2.0 * m, four_m = 4.0 * m, dm = (double)m;
+  const unsigned long long kFree = 1ULL << 63;
+
+  double cov[KD][D];
+#pragma unroll
+  for (int q = 0; q < D; ++q) {
+    const double* xr = P.x + q * P.ns + r0;
+    const double* xc = P.x + q * P.ns + c0;
+    const double mr = P.mu[q * Lp + r0];
+    double acc[KD], asum = 0.0;
+#pragma unroll
+    for (int d = 0; d < KD; ++d) acc[d] = 0.0;
+    for (int t = 0; t < m; ++t) {
+      const double a = xr[t] - mr;
+      asum += a;
+#pragma unroll
+      for (int d = 0; d < KD; ++d) acc[d] = fma(a, xc[t + d], acc[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < KD; ++d) cov[d][q] = fma(-P.mu[q * Lp + c0 + d], asum, acc[d]);
+  }
+  double2 cu[KD][D];
+  double ci[KD][D];
+  int cth[KD][D];
+#pragma unroll
+  for (int d = 0; d < KD - 1; ++d) {
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      cu[d][q] = P.U[q * Lp + c0 + d];
+      ci[d][q] = P.inv[q * Lp + c0 + d];
+      cth[d][q] = key_hi(P.keys + q * Lp, c0 + d);
+    }
+  }
+  for (int u = 0; u < it.nrows; u += KD) {
+#pragma unroll
+    for (int s = 0; s < KD; ++s) {
+      const long long i = r0 + u + s;
+      const int sin = (s + KD - 1) % KD;
+      const long long jn = c0 + u + s + KD - 1;
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        cu[sin][q] = P.U[q * Lp + jn];
+        ci[sin][q] = P.inv[q * Lp + jn];
+        cth[sin][q] = key_hi(P.keys + q * Lp, jn);
+      }
+      const bool step = (u + s) != 0;
+      double2 ru[D];
+      double ri[D];
+      int rth[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        ru[q] = step ? P.U[q * Lp + i] : make_double2(0.0, 0.0);
+        ri[q] = P.inv[q * Lp + i];
+        rth[q] = key_hi(P.keys + q * Lp, i);
+      }
+      double pk[KD][D];
+      bool fire = false;
+#pragma unroll
+      for (int d = 0; d < KD; ++d) {
+        const int sl = (s + d) % KD;
+        unsigned long long sk[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          cov[d][q] = fma(ru[q].x, cu[sl][q].y, cov[d][q]);
+          cov[d][q] = fma(ru[q].y, cu[sl][q].x, cov[d][q]);
+          const double a = ri[q], b = ci[sl][q];
+          double v = fma(-two_m, cov[d][q] * (a * b), two_m);
+          v = fmin(fmax(v, 0.0), four_m);
+          if (a == 0.0 || b == 0.0) v = (a == 0.0 && b == 0.0) ? 0.0 : dm;  // distance.hpp:14-15
+          sk[q] = (unsigned long long)__double_as_longlong(sqrt_search(v)) | (q >= P.n_must ? kFree : 0ULL);
+        }
+        sort_keys<D>(sk);
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          acc += __longlong_as_double((long long)(sk[q] & ~kFree));
+          pk[d][q] = acc * (1.0 / (double)(q + 1));
+          const int h = __double2hiint(pk[d][q]);
+          fire |= (h <= rth[q]) | (h <= cth[sl][q]);
+        }
+      }
+      if (__any_sync(0xffffffffu, fire)) {
+        long long best[D];
+#pragma unroll
+        for (int q = 0; q < D; ++q) best[q] = kNoKeyS;
+        const bool row_ok = i < L;
+#pragma unroll
+        for (int d = 0; d < KD; ++d) {
+          const int sl = (s + d) % KD;
+          const long long j = c0 + u + s + d;
+          if (row_ok && j < L) {
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+              const double pv = pk[d][q];
+              const int h = __double2hiint(pv);
+              if (h <= cth[sl][q]) {
+                red_min64(P.keys + q * Lp + j, pack_key(pv, i, P.imask));
+                cth[sl][q] = min(cth[sl][q], h);
+              }
+              if (h <= rth[q]) {
+                const long long kr = pack_key(pv, j, P.imask);
+                best[q] = kr < best[q] ? kr : best[q];
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < D; ++q) {
+          const long long b = warp_min64(best[q]);
+          if (lane == 0 && b != kNoKeyS) red_min64(P.keys + q * Lp + i, b);
+        }
       }
     }
   }
@@ -348,8 +611,8 @@ __global__ void k_mstomp_finalize(const MStompParams P, int D, int dims_out,
   const int kout = (int)(g / P.L);
   const long long i = g % P.L;
   const int kk = kout < D ? kout : D - 1;
-  const long long key = P.keys[kk * P.L + i];
-  const long long j = key == kNoKey ? -1 : (key & P.imask);
+  const long long key = P.keys[kk * P.Lp + i];
+  const long long j = key >= kNoKeyS ? -1 : (key & P.imask);
   double v = INFINITY;
   long long dim = -1;
   if (j >= 0) {
@@ -361,9 +624,9 @@ __global__ void k_mstomp_finalize(const MStompParams P, int D, int dims_out,
       if (ii == 0.0 || ij == 0.0) {
         d = (ii == 0.0 && ij == 0.0) ? 0.0 : sqrt((double)m);
       } else {
-        const double mi = P.mu[q * P.L + i], mj = P.mu[q * P.L + j];
-        const double* xi = P.x + q * P.n + i;
-        const double* xj = P.x + q * P.n + j;
+        const double mi = P.mu[q * P.Lp + i], mj = P.mu[q * P.Lp + j];
+        const double* xi = P.x + q * P.ns + i;
+        const double* xj = P.x + q * P.ns + j;
         double acc = 0.0;
         for (int t = lane; t < m; t += 32) {
           const double e = __dmul_rn(xi[t] - mi, ii) - __dmul_rn(xj[t] - mj, ij);
@@ -462,6 +725,47 @@ std::mutex g_multi_mu;  // calls are serialised (scratch is per call)
 
 }  // namespace
 
+namespace {
+
+template <int KD, int DIMS>
+void launch_simple(const SimpleParams& P, cudaStream_t st) {
+  k_simple_t<KD, DIMS><<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
+}
+
+void launch_simple_generic(const SimpleParams& P, cudaStream_t st) {
+  k_simple<<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
+}
+
+using SLaunch = void (*)(const SimpleParams&, cudaStream_t);
+
+SLaunch simple_launcher(int dims) {
+  // diagonals per lane by register budget (128 at 2 CTAs/SM); MPGPU_SIMPLE_KD
+  // overrides it for dims 1-2 (experiments)
+  const char* e = getenv("MPGPU_SIMPLE_KD");
+  const int kd = e ? atoi(e) : 0;
+  switch (dims) {
+    case 1: return kd == 8 ? launch_simple<8, 1> : (kd == 2 ? launch_simple<2, 1> : launch_simple<4, 1>);
+    case 2: return kd == 8 ? launch_simple<8, 2> : (kd == 2 ? launch_simple<2, 2> : launch_simple<4, 2>);
+    case 3: return launch_simple<2, 3>;
+    case 4: return launch_simple<2, 4>;
+    case 5: return launch_simple<1, 5>;
+    case 6: return launch_simple<1, 6>;
+    case 7: return launch_simple<1, 7>;
+    case 8: return launch_simple<1, 8>;
+    default: return launch_simple_generic;
+  }
+}
+
+int simple_kd(int dims) {
+  const char* e = getenv("MPGPU_SIMPLE_KD");
+  const int kd = e ? atoi(e) : 0;
+  if (dims <= 2) return (kd == 8 || kd == 2) ? kd : 4;
+  if (dims <= 4) return 2;
+  return 1;
+}
+
+}  // namespace
+
 extern "C" {
 
 mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
@@ -486,72 +790,91 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
 
   const long long na = A->n_a, nb = self ? na : A->n_b;
   const long long La = na - m + 1, Lb = nb - m + 1;
+  if (std::max(La, Lb) >= (1LL << 31)) return set_error(MPGPU_EUNSUPPORTED, "profile longer than 2^31");
+  const long long pad = kSimplePad;
+  const long long nsa = na + pad + m, nsb = nb + pad + m;   // padded strides
+  const long long Lpa = La + pad, Lpb = Lb + pad;
   DevMem mem;
   double *xa, *xb = nullptr, *xca, *xcb = nullptr, *nra, *nrb = nullptr, *shift;
   long long *k0, *k1;
   MM_CUDA(mem.alloc(&xa, dims * na));
-  MM_CUDA(mem.alloc(&xca, dims * na));
-  MM_CUDA(mem.alloc(&nra, La));
+  MM_CUDA(mem.alloc(&xca, dims * nsa));
+  MM_CUDA(mem.alloc(&nra, Lpa));
   MM_CUDA(mem.alloc(&shift, dims));
   MM_CUDA(cudaMemcpyAsync(xa, A->a, sizeof(double) * dims * na, cudaMemcpyHostToDevice, st));
   if (!self) {
     MM_CUDA(mem.alloc(&xb, dims * nb));
-    MM_CUDA(mem.alloc(&xcb, dims * nb));
-    MM_CUDA(mem.alloc(&nrb, Lb));
+    MM_CUDA(mem.alloc(&xcb, dims * nsb));
+    MM_CUDA(mem.alloc(&nrb, Lpb));
     MM_CUDA(cudaMemcpyAsync(xb, A->b, sizeof(double) * dims * nb, cudaMemcpyHostToDevice, st));
   }
   // shared per-dim shift: the mean of A's dimension (host, from the caller's buffer)
   std::vector<double> sh(dims);
   for (long long d = 0; d < dims; ++d) {
-    double s = 0.0;
-    for (long long t = 0; t < na; ++t) s += A->a[d * na + t];
-    sh[d] = s / (double)na;
+    double sm = 0.0;
+    for (long long t = 0; t < na; ++t) sm += A->a[d * na + t];
+    sh[d] = sm / (double)na;
   }
   MM_CUDA(cudaMemcpyAsync(shift, sh.data(), sizeof(double) * dims, cudaMemcpyHostToDevice, st));
   // self: k0 = right keys (row candidates), k1 = left keys (column candidates)
   // AB:   k0 = A keys, k1 = B keys
-  MM_CUDA(mem.alloc(&k0, La));
-  MM_CUDA(mem.alloc(&k1, self ? La : Lb));
+  const long long Lk1 = self ? La : Lb, Lpk1 = self ? Lpa : Lpb;
+  MM_CUDA(mem.alloc(&k0, Lpa));
+  MM_CUDA(mem.alloc(&k1, Lpk1));
   const int index_bits = std::max(1, ceil_log2ll(std::max(La, Lb)));
   const long long imask = (1LL << index_bits) - 1;
 
+  // compile-time dims / diagonals per lane up to 16 dims, else the generic kernel
+  const int KD = simple_kd((int)dims);
+  const bool generic = dims > 8;
+  const int band = generic ? 32 : 32 * KD;
   std::vector<MItem> items;
-  const long long seg = seg_rows(m, std::max(La, Lb));
+  const long long seg = std::max<long long>(1024, 8 * m);
+  auto build = [&](int pass, long long klo, long long khi, long long LR, long long LC) {
+    for (long long kb = klo; kb < khi; kb += band) {
+      const long long rows = std::min(LR, LC - kb);
+      for (long long r0 = 0; r0 < rows; r0 += seg) {
+        long long nr = std::min(seg, rows - r0);
+        if (!generic) nr = (nr + KD - 1) / KD * KD;  // whole KD-step groups (padding covers the tail)
+        items.push_back(MItem{kb, r0, (int)nr, pass});
+      }
+    }
+  };
   SimpleParams P{};
   P.dims = (int)dims;
   P.m = (int)m;
   P.imask = imask;
-  RawSeries RA{xca, nra, na, La}, RB{xcb, nrb, nb, Lb};
+  RawSeries RA{xca, nra, na, nsa, La}, RB{xcb, nrb, nb, nsb, Lb};
   if (self) {
-    if (A->zone + 1 < La) build_mitems(items, 0, A->zone + 1, La, La, La, seg);
+    if (A->zone + 1 < La) build(0, A->zone + 1, La, La, La);
     P.pass[0] = SimplePass{RA, RA, A->zone + 1, La, k0, k1};
   } else {
     // pass 0: rows = B windows, columns = A windows (k >= 0); pass 1: rows = A, columns = B (k >= 1)
-    build_mitems(items, 0, 0, La, Lb, La, seg);
-    if (Lb > 1) build_mitems(items, 1, 1, Lb, La, Lb, seg);
+    build(0, 0, La, Lb, La);
+    if (Lb > 1) build(1, 1, Lb, La, Lb);
     P.pass[0] = SimplePass{RB, RA, 0, La, k1, k0};
     P.pass[1] = SimplePass{RA, RB, 1, Lb, k0, k1};
   }
   sort_mitems(items);
   MItem* d_items = nullptr;
   MM_CUDA(mem.alloc(&d_items, items.size()));
-  MM_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(MItem) * items.size(),
-                          cudaMemcpyHostToDevice, st));
+  if (!items.empty())
+    MM_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(MItem) * items.size(),
+                            cudaMemcpyHostToDevice, st));
   P.items = d_items;
   P.n_items = (long long)items.size();
 
   MM_CUDA(cudaEventRecord(tm.a, st));
   const int bs = 256;
-  k_center<<<(unsigned)((dims * na + bs - 1) / bs), bs, 0, st>>>(xa, na, (int)dims, shift, xca);
-  k_raw_energy<<<(unsigned)((La + bs - 1) / bs), bs, 0, st>>>(xca, na, La, (int)dims, (int)m, nra);
+  k_center<<<(unsigned)((dims * nsa + bs - 1) / bs), bs, 0, st>>>(xa, na, nsa, (int)dims, shift, xca);
+  k_raw_energy<<<(unsigned)((Lpa + bs - 1) / bs), bs, 0, st>>>(xca, nsa, La, Lpa, (int)dims, (int)m, nra);
   if (!self) {
-    k_center<<<(unsigned)((dims * nb + bs - 1) / bs), bs, 0, st>>>(xb, nb, (int)dims, shift, xcb);
-    k_raw_energy<<<(unsigned)((Lb + bs - 1) / bs), bs, 0, st>>>(xcb, nb, Lb, (int)dims, (int)m, nrb);
+    k_center<<<(unsigned)((dims * nsb + bs - 1) / bs), bs, 0, st>>>(xb, nb, nsb, (int)dims, shift, xcb);
+    k_raw_energy<<<(unsigned)((Lpb + bs - 1) / bs), bs, 0, st>>>(xcb, nsb, Lb, Lpb, (int)dims, (int)m, nrb);
   }
-  k_fill<<<(unsigned)((La + bs - 1) / bs), bs, 0, st>>>(k0, La);
-  k_fill<<<(unsigned)(((self ? La : Lb) + bs - 1) / bs), bs, 0, st>>>(k1, self ? La : Lb);
-  if (P.n_items > 0)
-    k_simple<<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
+  k_fill_val<<<(unsigned)((Lpa + bs - 1) / bs), bs, 0, st>>>(k0, La, Lpa, kNoKeyS, kPadKey);
+  k_fill_val<<<(unsigned)((Lpk1 + bs - 1) / bs), bs, 0, st>>>(k1, Lk1, Lpk1, kNoKeyS, kPadKey);
+  if (P.n_items > 0) simple_launcher((int)dims)(P, st);
   const unsigned fa = (unsigned)((La * 32 + bs - 1) / bs);
   MM_CUDA(cudaGetLastError());
   // outputs land in device scratch, then host
@@ -597,24 +920,35 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
 
 namespace {
 
+template <int KD, int D>
+void launch_mstomp_t(const MStompParams& P, cudaStream_t st) {
+  k_mstomp_t<KD, D><<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
+}
+
 template <int D>
 void launch_mstomp(const MStompParams& P, cudaStream_t st) {
-  if (P.n_items > 0)
-    k_mstomp<D><<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
+  k_mstomp<D><<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
 }
 
 using MLaunch = void (*)(const MStompParams&, cudaStream_t);
 
+// diagonals per lane by register budget (the generic kernels above 8 dims walk one)
+int mstomp_kd(int D) {
+  if (D == 1) return 4;
+  if (D <= 4) return 2;
+  return 1;
+}
+
 MLaunch mstomp_launcher(int D) {
   switch (D) {
-    case 1: return launch_mstomp<1>;
-    case 2: return launch_mstomp<2>;
-    case 3: return launch_mstomp<3>;
-    case 4: return launch_mstomp<4>;
-    case 5: return launch_mstomp<5>;
-    case 6: return launch_mstomp<6>;
-    case 7: return launch_mstomp<7>;
-    case 8: return launch_mstomp<8>;
+    case 1: return launch_mstomp_t<4, 1>;
+    case 2: return launch_mstomp_t<2, 2>;
+    case 3: return launch_mstomp_t<2, 3>;
+    case 4: return launch_mstomp_t<2, 4>;
+    case 5: return launch_mstomp_t<1, 5>;
+    case 6: return launch_mstomp_t<1, 6>;
+    case 7: return launch_mstomp_t<1, 7>;
+    case 8: return launch_mstomp_t<1, 8>;
     default: break;
   }
   if (D <= 12) return launch_mstomp<12>;
@@ -671,28 +1005,43 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
   MM_CUDA(cudaEventCreate(&tm.b));
 
   const long long L = n - m + 1, pad = mpgpu_internal::stats_pad(), Lp = L + pad;
+  const long long ns = n + pad;
+  if (L >= (1LL << 31)) return set_error(MPGPU_EUNSUPPORTED, "profile longer than 2^31");
   DevMem mem;
   double *x, *mu, *inv, *omp;
   double2* U;
   long long *keys, *opi, *odo;
   int* dperm;
-  MM_CUDA(mem.alloc(&x, (size_t)D * n));
-  MM_CUDA(mem.alloc(&mu, (size_t)D * L));
+  MM_CUDA(mem.alloc(&x, (size_t)D * ns));
+  MM_CUDA(mem.alloc(&mu, (size_t)D * Lp));
   MM_CUDA(mem.alloc(&inv, (size_t)D * Lp));
   MM_CUDA(mem.alloc(&U, (size_t)D * Lp));
-  MM_CUDA(mem.alloc(&keys, (size_t)D * L));
+  MM_CUDA(mem.alloc(&keys, (size_t)D * Lp));
   MM_CUDA(mem.alloc(&omp, (size_t)dims * L));
   MM_CUDA(mem.alloc(&opi, (size_t)dims * L));
   MM_CUDA(mem.alloc(&odo, (size_t)dims * L));
   MM_CUDA(mem.alloc(&dperm, D));
+  MM_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * D * ns, st));
+  MM_CUDA(cudaMemsetAsync(mu, 0, sizeof(double) * D * Lp, st));
   for (int q = 0; q < D; ++q)
-    MM_CUDA(cudaMemcpyAsync(x + (size_t)q * n, A->x + (size_t)perm[q] * n, sizeof(double) * n,
+    MM_CUDA(cudaMemcpyAsync(x + (size_t)q * ns, A->x + (size_t)perm[q] * n, sizeof(double) * n,
                             cudaMemcpyHostToDevice, st));
   MM_CUDA(cudaMemcpyAsync(dperm, perm.data(), sizeof(int) * D, cudaMemcpyHostToDevice, st));
   const int index_bits = std::max(1, ceil_log2ll(L));
   const long long imask = (1LL << index_bits) - 1;
+  const int KD = mstomp_kd(D);
   std::vector<MItem> items;
-  if (A->zone + 1 < L) build_mitems(items, 0, A->zone + 1, L, L, L, seg_rows(m, L));
+  if (A->zone + 1 < L) {
+    const long long band = 32LL * KD, seg = std::max<long long>(1024, 8 * m);
+    for (long long kb = A->zone + 1; kb < L; kb += band) {
+      const long long rows = L - kb;
+      for (long long r0 = 0; r0 < rows; r0 += seg) {
+        long long nr = std::min(seg, rows - r0);
+        nr = (nr + KD - 1) / KD * KD;  // whole KD-step groups (padding covers the tail)
+        items.push_back(MItem{kb, r0, (int)nr, 0});
+      }
+    }
+  }
   sort_mitems(items);
   MItem* d_items = nullptr;
   MM_CUDA(mem.alloc(&d_items, items.size()));
@@ -702,18 +1051,20 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
 
   MStompParams P{};
   P.x = x; P.mu = mu; P.inv = inv; P.U = U;
-  P.n = n; P.L = L; P.Lp = Lp; P.khi = L;
+  P.n = n; P.ns = ns; P.L = L; P.Lp = Lp; P.khi = L;
   P.keys = keys; P.items = d_items; P.n_items = (long long)items.size();
   P.m = (int)m; P.n_must = n_must; P.D = D; P.imask = imask;
 
   MM_CUDA(cudaEventRecord(tm.a, st));
   for (int q = 0; q < D; ++q)
-    MM_CUDA(mpgpu_internal::series_stats(x + (size_t)q * n, n, (int)m, mu + (size_t)q * L,
+    MM_CUDA(mpgpu_internal::series_stats(x + (size_t)q * ns, n, (int)m, mu + (size_t)q * Lp,
                                          inv + (size_t)q * Lp, U + (size_t)q * Lp, nullptr, st));
   const int bs = 256;
-  k_fill<<<(unsigned)(((long long)D * L + bs - 1) / bs), bs, 0, st>>>(keys, (long long)D * L);
+  for (int q = 0; q < D; ++q)
+    k_fill_val<<<(unsigned)((Lp + bs - 1) / bs), bs, 0, st>>>(keys + (size_t)q * Lp, L, Lp, kNoKeyS,
+                                                              kPadKey);
   MM_CUDA(cudaGetLastError());
-  mstomp_launcher(D)(P, st);
+  if (P.n_items > 0) mstomp_launcher(D)(P, st);
   MM_CUDA(cudaGetLastError());
   const long long outs = (long long)dims * L;
   k_mstomp_finalize<<<(unsigned)((outs * 32 + bs - 1) / bs), bs, 0, st>>>(P, D, (int)dims, dperm,

@@ -1,6 +1,7 @@
-// C++ shim: the reference's mprof::stomp / mprof::scrimp signatures
-// (profile.hpp:80-89) on top of the C ABI (include/mprof_gpu.h). Status codes
+// C++ shim: the reference's mprof::stomp / scrimp / mstomp / simple_join
+// signatures (profile.hpp:80-100) on top of the C ABI (include/mprof_gpu.h). Status codes
 // come back as the reference's exception types (error.hpp:9-19).
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <utility>
@@ -17,6 +18,15 @@ TimeSeries::TimeSeries(std::vector<double> values) : data_(std::move(values)) {
   for (std::size_t i = 0; i < data_.size(); ++i)
     if (!std::isfinite(data_[i]))
       throw ParameterError("time series sample " + std::to_string(i) + " is not finite");
+}
+
+MultiTimeSeries::MultiTimeSeries(std::vector<TimeSeries> dims) : dims_(std::move(dims)) {
+  if (dims_.empty()) throw ParameterError("multivariate series needs at least one dimension");
+  const Index n = dims_.front().size();
+  for (std::size_t k = 1; k < dims_.size(); ++k)
+    if (dims_[k].size() != n)
+      throw ParameterError("dimension " + std::to_string(k) + " has length " +
+                           std::to_string(dims_[k].size()) + ", expected " + std::to_string(n));
 }
 
 const char *mode_name(Mode mode) {
@@ -161,6 +171,103 @@ MatrixProfile scrimp(const TimeSeries &ts_a, Index window, double ez_fraction, I
     mp.left_index.swap(left);
     mp.right_index.swap(right);
   }
+  if (progress) progress(1.0);
+  return mp;
+}
+
+namespace {
+
+std::vector<double> dim_major(const MultiTimeSeries &m) {
+  const std::size_t n = static_cast<std::size_t>(m.size());
+  std::vector<double> x(n * static_cast<std::size_t>(m.dims()));
+  for (Index d = 0; d < m.dims(); ++d)
+    std::copy(m.dim(d).values().begin(), m.dim(d).values().end(), x.begin() + d * n);
+  return x;
+}
+
+}  // namespace
+
+MultiMatrixProfile mstomp(const MultiTimeSeries &mts, Index window, double ez_fraction,
+                          const std::vector<Index> &must_dims, const std::vector<Index> &exc_dims,
+                          int n_workers, const ProgressFn &progress) {
+  if (n_workers < 1) throw ParameterError("n_workers must be >= 1");
+  check_window(window, mts.size(), "series");
+  const Index zone = zone_size(window, ez_fraction);
+  const Index d = mts.dims(), L = mts.size() - window + 1;
+  const std::vector<double> x = dim_major(mts);
+  std::vector<double> v(static_cast<std::size_t>(d * L));
+  std::vector<Index> pi(v.size()), dorder(v.size());
+  mpgpu_mstomp_args args{};
+  args.x = x.data();
+  args.n = mts.size();
+  args.dims = d;
+  args.window = window;
+  args.zone = zone;
+  args.must_dims = must_dims.data();
+  args.n_must = static_cast<int64_t>(must_dims.size());
+  args.exc_dims = exc_dims.data();
+  args.n_exc = static_cast<int64_t>(exc_dims.size());
+  args.mp = v.data();
+  args.pi = pi.data();
+  args.dim_order = dorder.data();
+  const mpgpu_status st = mpgpu_mstomp(&args);
+  if (st != MPGPU_OK) raise(st);
+  MultiMatrixProfile r;
+  r.window = window;
+  r.exclusion_zone = zone;
+  r.must_dims = must_dims;
+  r.exc_dims = exc_dims;
+  r.data_len = mts.size();
+  r.data_dims = d;
+  for (Index k = 0; k < d; ++k) {
+    r.values.emplace_back(v.begin() + k * L, v.begin() + (k + 1) * L);
+    r.index.emplace_back(pi.begin() + k * L, pi.begin() + (k + 1) * L);
+    r.dim_order.emplace_back(dorder.begin() + k * L, dorder.begin() + (k + 1) * L);
+  }
+  if (progress) progress(1.0);
+  return r;
+}
+
+MatrixProfile simple_join(const MultiTimeSeries &mts_a, const MultiTimeSeries *mts_b,
+                          Index window, double ez_fraction, const ProgressFn &progress) {
+  if (mts_b && mts_b->dims() != mts_a.dims())
+    throw ParameterError("dimension mismatch: " + std::to_string(mts_a.dims()) + " vs " +
+                         std::to_string(mts_b->dims()));
+  check_window(window, mts_a.size(), "series");
+  if (mts_b) check_window(window, mts_b->size(), "series B");
+  const Index zone = mts_b ? 0 : zone_size(window, ez_fraction);
+  const Index La = mts_a.size() - window + 1;
+  const std::vector<double> xa = dim_major(mts_a);
+  std::vector<double> xb;
+  if (mts_b) xb = dim_major(*mts_b);
+  MatrixProfile mp;
+  mp.window = window;
+  mp.exclusion_zone = zone;
+  mp.mode = Mode::simple;
+  mp.join_kind = mts_b ? JoinKind::ab : JoinKind::self;
+  mp.data_len = mts_a.size();
+  mp.data_len_b = mts_b ? mts_b->size() : 0;
+  mp.data_dims = mts_a.dims();
+  mp.values.resize(La);
+  mp.index.resize(La);
+  mpgpu_simple_args args{};
+  args.a = xa.data();
+  args.n_a = mts_a.size();
+  args.b = mts_b ? xb.data() : nullptr;
+  args.n_b = mts_b ? mts_b->size() : 0;
+  args.dims = mts_a.dims();
+  args.window = window;
+  args.zone = zone;
+  args.mp_a = mp.values.data();
+  args.pi_a = mp.index.data();
+  if (!mts_b) {
+    mp.left_index.resize(La);
+    mp.right_index.resize(La);
+    args.left_a = mp.left_index.data();
+    args.right_a = mp.right_index.data();
+  }
+  const mpgpu_status st = mpgpu_simple_join(&args);
+  if (st != MPGPU_OK) raise(st);
   if (progress) progress(1.0);
   return mp;
 }

@@ -133,3 +133,20 @@ def test_cpp_headers_compile():
     r = subprocess.run([gxx, "-std=c++20", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"), src],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_multivariate_parameter_errors_without_gpu(mp):
+    """mpgpu_mstomp / mpgpu_simple_join reject bad arguments (SPEC.md:229,
+    :240) before any device work, as the reference's ParameterError."""
+    x = np.random.default_rng(1).standard_normal((3, 64))
+    for must, exc in (((0,), (0,)), ((), (0, 1, 2)), ((3,), ()), ((0, 0), ()), ((), (-1,))):
+        with pytest.raises(mp.ParameterError):
+            mp.mstomp(x, 8, 0.5, must, exc)
+    with pytest.raises(mp.ParameterError):
+        mp.simple_join(x, x[:2], 8)
+    with pytest.raises(mp.ParameterError):
+        mp.mstomp(x, 65, 0.5)
+    with pytest.raises(mp.ParameterError):
+        mp.MultiTimeSeries([x[0], x[1][:50]])
+    with pytest.raises(mp.ParameterError):
+        mp.MultiTimeSeries([])

@@ -101,3 +101,38 @@ def test_cpp_scrimp_anytime(exe, tmp_path, oracle_lib):
     ref_mp, ref_pi = oracle_lib.scrimp_diagonals(x, w, mp.band_diagonals(bands, L, zone))
     assert close(res["mp"], ref_mp)[0]
     assert not index_mismatches(res["pi"], ref_pi, np.arange(L), x, x, w)
+
+
+def test_cpp_simple_and_mstomp(exe, tmp_path, oracle_lib):
+    """mprof::simple_join / mprof::mstomp (profile.hpp:91-100) from a C++ caller."""
+    from tests.parity import mstomp_mismatches, raw_index_mismatches
+    g = np.random.default_rng(13)
+    x = np.cumsum(g.standard_normal((3, 1500)), axis=1)
+    w = 32
+    rc, info, res = _run(exe, tmp_path, x.ravel(), w, 0.5, "simple", extra=(3,))
+    assert rc == 0 and info["mode"] == "simple" and info["dims"] == 3 and info["zone"] == 16
+    ref = oracle_lib.simple_join(x, None, w, 0.5, n_workers=4)
+    assert close(res["mp"], ref[0])[0]
+    assert not raw_index_mismatches(res["pi"], ref[1], np.arange(ref[0].size), x, x, w)
+    y = np.cumsum(g.standard_normal((3, 700)), axis=1)
+    by = tmp_path / "y.f64"
+    y.tofile(by)
+    rc, info, res = _run(exe, tmp_path, x.ravel(), w, 0.5, "simple", extra=(3, by))
+    assert rc == 0 and info["join"] == "ab" and res["left"].size == 0
+    ref = oracle_lib.simple_join(x, y, w)
+    assert close(res["mp"], ref[0])[0]
+    # mstomp with a must dim and an excluded dim
+    inp = tmp_path / "m.f64"
+    x.tofile(inp)
+    args = [exe, str(inp), str(w), "0.5", str(tmp_path / "mo"), "mstomp", "3", "2", "0"]
+    r = subprocess.run(args, capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    L = x.shape[1] - w + 1
+    got = tuple(np.fromfile(tmp_path / f"mo.{k}", dtype=np.float64 if k == "mp" else np.int64)
+                .reshape(3, L) for k in ("mp", "pi", "dim"))
+    ref = oracle_lib.mstomp(x, w, 0.5, (2,), (0,), n_workers=4)
+    assert not mstomp_mismatches(got, ref, x, w, (2,), (0,))
+    # overlapping must / exc -> ParameterError (SPEC.md:229)
+    args[-2:] = ["1", "1"]
+    r = subprocess.run(args, capture_output=True, text=True)
+    assert r.returncode == 2 and "ParameterError" in r.stdout
