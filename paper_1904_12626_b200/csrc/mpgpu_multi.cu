@@ -73,13 +73,21 @@ __device__ __forceinline__ long long warp_min64(long long v) {
 // sqrt for the search (s >= 0): MUFU reciprocal square root + one Newton step
 // (relative error ~1e-13; the reported values are recomputed exactly).
 __device__ __forceinline__ double sqrt_search(double s) {
-  const double s2 = fmax(s, 1e-300);
+  const double s2 = s + 1e-300;  // s >= 0: keeps rsqrt finite at 0
   double y;
   asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(s2));
   const double h = 0.5 * s2;
   const double e = fma(-h * y, y, 0.5);
   y = fma(y, e, y);
   return s * y;
+}
+
+// max(v, 0) on the integer pipe: a negative value (rounding residue of a
+// perfect match) gets its high word zeroed, leaving a tiny non-negative
+// denormal that the search treats as 0.
+__device__ __forceinline__ double clamp0(double v) {
+  const int h = __double2hiint(v);
+  return __hiloint2double(h < 0 ? 0 : h, __double2loint(v));
 }
 
 // ---- SiMPle ------------------------------------------------------------------
@@ -330,6 +338,23 @@ __global__ void k_fill_val(long long* k, long long len, long long total, long lo
   if (i < total) k[i] = i < len ? v : pad;
 }
 
+// blocked interleave of the mSTOMP statistics (mblk): WU = {df, dg}, WI =
+// {inv, 0.5 when window j of dim q is flat}; keys filled alongside (kNoKeyS,
+// kPadKey past the last window)
+__global__ void k_build_w(const double2* __restrict__ U, const double* __restrict__ inv,
+                          long long L, long long Lp, long long Lb, int D, double2* __restrict__ WU,
+                          double2* __restrict__ WI, long long* __restrict__ keys) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Lb * D) return;
+  const long long blk = t / (32LL * D);
+  const int q = (int)((t / 32) % D);
+  const long long j = blk * 32 + (t & 31);
+  const double a = j < Lp ? inv[q * Lp + j] : 0.0;
+  WU[t] = j < Lp ? U[q * Lp + j] : make_double2(0.0, 0.0);
+  WI[t] = make_double2(a, (j < L && a == 0.0) ? 0.5 : 0.0);
+  keys[t] = j < L ? kNoKeyS : kPadKey;
+}
+
 // per-dim centring by a shared shift (distances are shift-invariant) into a
 // zero-padded layout of stride ns
 __global__ void k_center(const double* __restrict__ x, long long n, long long ns, int dims,
@@ -364,15 +389,24 @@ struct MStompParams {
   const double* mu;   // D x Lp (zero padded)
   const double* inv;  // D x Lp (0: flat / padding)
   const double2* U;   // D x Lp
+  // blocked layout [j / 32][q][j % 32] (mblk): a warp's 32 consecutive windows
+  // are one contiguous run per dim, and dim q sits at the constant offset 32 q
+  const double2* WU;  // {df, dg}
+  const double2* WI;  // {inv, 0.5 if the window is flat else 0}
   long long n, ns, L, Lp;
   long long khi;      // diagonals [klo, khi) = [zone + 1, L)
-  long long* keys;    // D x Lp: kNoKeyS when empty, kPadKey in the padding
+  long long* keys;    // blocked like WU: kNoKeyS when empty, kPadKey in the padding
   const MItem* items;
   long long n_items;
   int m, n_must;
   int D;              // admissible dims (<= the kernel's capacity)
   long long imask;
 };
+
+// element index of (window j, dim 0) in the blocked layout; dim q adds 32 q
+__device__ __forceinline__ long long mblk(long long j, int D) {
+  return ((j >> 5) * D << 5) + (j & 31);
+}
 
 // stable odd-even transposition sort of D unsigned keys (ascending)
 template <int D>
@@ -400,7 +434,7 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mstomp(const MStompParams P) {
   long long rend = min(r0 + it.nrows, P.L - k);
   if (k >= P.khi || rend < r0) rend = r0;
   const int m = P.m;
-  const double two_m = 2.0 * m, four_m = 4.0 * m, dm = (double)m;
+  const double two_m = 2.0 * m;
 
   double cov[D];
 #pragma unroll
@@ -421,46 +455,44 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mstomp(const MStompParams P) {
   }
   const unsigned long long kFree = 1ULL << 63;  // sorts free dims after the must dims
   const long long rmax = __reduce_max_sync(0xffffffffu, (unsigned)(rend - r0)) + r0;
+  const int Dr = P.D;
   for (long long i = r0; i < rmax; ++i) {
     const bool live = i < rend;
     const long long j = live ? i + k : i;  // dead lanes read a valid column
+    const long long ei = mblk(i, Dr), ej = mblk(j, Dr);
     unsigned long long s[D];
 #pragma unroll
     for (int q = 0; q < D; ++q) {
-      if (q >= P.D) {  // capacity padding: sorts last, never reaches a key
+      if (q >= Dr) {  // capacity padding: sorts last, never reaches a key
         s[q] = ~0ULL;
         continue;
       }
-      const long long oi = q * P.Lp + i, oj = q * P.Lp + j;
       if (i > r0) {
-        const double2 ru = P.U[oi], cu = P.U[oj];
+        const double2 ru = P.WU[ei + 32 * q], cu = P.WU[ej + 32 * q];
         cov[q] = fma(ru.x, cu.y, cov[q]);
         cov[q] = fma(ru.y, cu.x, cov[q]);
       }
-      const double ri = P.inv[oi], ci = P.inv[oj];
-      double v = fma(-two_m, cov[q] * (ri * ci), two_m);
-      v = fmin(fmax(v, 0.0), four_m);
-      if (ri == 0.0 || ci == 0.0) v = (ri == 0.0 && ci == 0.0) ? 0.0 : dm;  // distance.hpp:14-15
-      const double dist = sqrt_search(v);
-      s[q] = (unsigned long long)__double_as_longlong(dist) | (q >= P.n_must ? kFree : 0ULL);
+      const double2 ri = P.WI[ei + 32 * q], ci = P.WI[ej + 32 * q];
+      const double corr = fma(cov[q], ri.x * ci.x, ri.y + ci.y);  // flat convention via the halves
+      s[q] = (unsigned long long)__double_as_longlong(sqrt_search(clamp0(fma(-two_m, corr, two_m)))) |
+             (q >= P.n_must ? kFree : 0ULL);
     }
     sort_keys<D>(s);
     double acc = 0.0;
 #pragma unroll
     for (int q = 0; q < D; ++q) {
-      if (q >= P.D) break;
+      if (q >= Dr) break;
       acc += __longlong_as_double((long long)(s[q] & ~kFree));
       const double pk = acc * (1.0 / (double)(q + 1));
-      long long* kq = P.keys + q * P.Lp;
       const long long kr = live ? pack_key(pk, j, P.imask) : kNoKey;
       if (live) {
         const long long kc = pack_key(pk, i, P.imask);
-        if (kc < kq[j]) red_min64(&kq[j], kc);
+        if (kc < P.keys[ej + 32 * q]) red_min64(&P.keys[ej + 32 * q], kc);
       }
-      const long long tr = kq[i];
+      const long long tr = P.keys[ei + 32 * q];
       if (__any_sync(0xffffffffu, kr < tr)) {
         const long long b = warp_min64(kr);
-        if (lane == 0 && b < tr) red_min64(&kq[i], b);
+        if (lane == 0 && b < tr) red_min64(&P.keys[ei + 32 * q], b);
       }
     }
   }
@@ -483,7 +515,7 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
   const long long c0 = r0 + it.kb + (long long)lane * KD;
   const long long Lp = P.Lp, L = P.L;
   const int m = P.m;
-  const double two_m = 2.0 * m, four_m = 4.0 * m, dm = (double)m;
+  const double two_m = 2.0 * m;
   const unsigned long long kFree = 1ULL << 63;
 
   double cov[KD][D];
@@ -504,16 +536,18 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
 #pragma unroll
     for (int d = 0; d < KD; ++d) cov[d][q] = fma(-P.mu[q * Lp + c0 + d], asum, acc[d]);
   }
-  double2 cu[KD][D];
-  double ci[KD][D];
+  // column window: {df, dg}, {inv, flat half} and the D column thresholds
+  double2 cu[KD][D], ci[KD][D];
   int cth[KD][D];
+  const int* khi_ = reinterpret_cast<const int*>(P.keys) + 1;  // hi words
 #pragma unroll
   for (int d = 0; d < KD - 1; ++d) {
+    const long long e = mblk(c0 + d, D);
 #pragma unroll
     for (int q = 0; q < D; ++q) {
-      cu[d][q] = P.U[q * Lp + c0 + d];
-      ci[d][q] = P.inv[q * Lp + c0 + d];
-      cth[d][q] = key_hi(P.keys + q * Lp, c0 + d);
+      cu[d][q] = P.WU[e + 32 * q];
+      ci[d][q] = P.WI[e + 32 * q];
+      cth[d][q] = khi_[2 * (e + 32 * q)];
     }
   }
   for (int u = 0; u < it.nrows; u += KD) {
@@ -521,22 +555,24 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
     for (int s = 0; s < KD; ++s) {
       const long long i = r0 + u + s;
       const int sin = (s + KD - 1) % KD;
-      const long long jn = c0 + u + s + KD - 1;
+      {
+        const long long e = mblk(c0 + u + s + KD - 1, D);  // entering column
 #pragma unroll
-      for (int q = 0; q < D; ++q) {
-        cu[sin][q] = P.U[q * Lp + jn];
-        ci[sin][q] = P.inv[q * Lp + jn];
-        cth[sin][q] = key_hi(P.keys + q * Lp, jn);
+        for (int q = 0; q < D; ++q) {
+          cu[sin][q] = P.WU[e + 32 * q];
+          ci[sin][q] = P.WI[e + 32 * q];
+          cth[sin][q] = khi_[2 * (e + 32 * q)];
+        }
       }
       const bool step = (u + s) != 0;
-      double2 ru[D];
-      double ri[D];
+      double2 ru[D], ri[D];
       int rth[D];
+      const long long ei = mblk(i, D);
 #pragma unroll
       for (int q = 0; q < D; ++q) {
-        ru[q] = step ? P.U[q * Lp + i] : make_double2(0.0, 0.0);
-        ri[q] = P.inv[q * Lp + i];
-        rth[q] = key_hi(P.keys + q * Lp, i);
+        ru[q] = step ? P.WU[ei + 32 * q] : make_double2(0.0, 0.0);
+        ri[q] = P.WI[ei + 32 * q];
+        rth[q] = khi_[2 * (ei + 32 * q)];
       }
       double pk[KD][D];
       bool fire = false;
@@ -548,11 +584,11 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
         for (int q = 0; q < D; ++q) {
           cov[d][q] = fma(ru[q].x, cu[sl][q].y, cov[d][q]);
           cov[d][q] = fma(ru[q].y, cu[sl][q].x, cov[d][q]);
-          const double a = ri[q], b = ci[sl][q];
-          double v = fma(-two_m, cov[d][q] * (a * b), two_m);
-          v = fmin(fmax(v, 0.0), four_m);
-          if (a == 0.0 || b == 0.0) v = (a == 0.0 && b == 0.0) ? 0.0 : dm;  // distance.hpp:14-15
-          sk[q] = (unsigned long long)__double_as_longlong(sqrt_search(v)) | (q >= P.n_must ? kFree : 0ULL);
+          // corr with the flat convention (distance.hpp:14-15): inv = 0 for a flat
+          // window and the halves add 1 (both flat: d = 0) or 1/2 (one: d = sqrt(m))
+          const double corr = fma(cov[d][q], ri[q].x * ci[sl][q].x, ri[q].y + ci[sl][q].y);
+          sk[q] = (unsigned long long)__double_as_longlong(sqrt_search(clamp0(fma(-two_m, corr, two_m)))) |
+                  (q >= P.n_must ? kFree : 0ULL);
         }
         sort_keys<D>(sk);
         double acc = 0.0;
@@ -579,12 +615,12 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
               const double pv = pk[d][q];
               const int h = __double2hiint(pv);
               if (h <= cth[sl][q]) {
-                red_min64(P.keys + q * Lp + j, pack_key(pv, i, P.imask));
+                red_min64(P.keys + mblk(j, D) + 32 * q, pack_key(pv, i, P.imask));
                 cth[sl][q] = min(cth[sl][q], h);
               }
               if (h <= rth[q]) {
-                const long long kr = pack_key(pv, j, P.imask);
-                best[q] = kr < best[q] ? kr : best[q];
+                const long long kk = pack_key(pv, j, P.imask);
+                best[q] = kk < best[q] ? kk : best[q];
               }
             }
           }
@@ -592,7 +628,7 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
 #pragma unroll
         for (int q = 0; q < D; ++q) {
           const long long b = warp_min64(best[q]);
-          if (lane == 0 && b != kNoKeyS) red_min64(P.keys + q * Lp + i, b);
+          if (lane == 0 && b != kNoKeyS) red_min64(P.keys + ei + 32 * q, b);
         }
       }
     }
@@ -611,7 +647,7 @@ __global__ void k_mstomp_finalize(const MStompParams P, int D, int dims_out,
   const int kout = (int)(g / P.L);
   const long long i = g % P.L;
   const int kk = kout < D ? kout : D - 1;
-  const long long key = P.keys[kk * P.Lp + i];
+  const long long key = P.keys[mblk(i, D) + 32 * kk];
   const long long j = key >= kNoKeyS ? -1 : (key & P.imask);
   double v = INFINITY;
   long long dim = -1;
@@ -932,19 +968,27 @@ void launch_mstomp(const MStompParams& P, cudaStream_t st) {
 
 using MLaunch = void (*)(const MStompParams&, cudaStream_t);
 
-// diagonals per lane by register budget (the generic kernels above 8 dims walk one)
+// diagonals per lane by register budget (the generic kernels above 8 dims walk
+// one); MPGPU_MSTOMP_KD overrides it for D <= 4 (experiments)
 int mstomp_kd(int D) {
-  if (D == 1) return 4;
-  if (D <= 4) return 2;
-  return 1;
+  const char* e = getenv("MPGPU_MSTOMP_KD");
+  const int kd = e ? atoi(e) : 0;
+  if (D <= 4 && (kd == 1 || kd == 2 || kd == 4)) return kd;
+  return D <= 3 ? 2 : 1;  // measured (tools/bench_multi.py): KD = 4 spills from D = 2 on
+}
+
+template <int D>
+MLaunch mstomp_pick(int kd) {
+  return kd == 4 ? launch_mstomp_t<4, D> : (kd == 2 ? launch_mstomp_t<2, D> : launch_mstomp_t<1, D>);
 }
 
 MLaunch mstomp_launcher(int D) {
+  const int kd = mstomp_kd(D);
   switch (D) {
-    case 1: return launch_mstomp_t<4, 1>;
-    case 2: return launch_mstomp_t<2, 2>;
-    case 3: return launch_mstomp_t<2, 3>;
-    case 4: return launch_mstomp_t<2, 4>;
+    case 1: return mstomp_pick<1>(kd);
+    case 2: return mstomp_pick<2>(kd);
+    case 3: return mstomp_pick<3>(kd);
+    case 4: return mstomp_pick<4>(kd);
     case 5: return launch_mstomp_t<1, 5>;
     case 6: return launch_mstomp_t<1, 6>;
     case 7: return launch_mstomp_t<1, 7>;
@@ -1016,7 +1060,11 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
   MM_CUDA(mem.alloc(&mu, (size_t)D * Lp));
   MM_CUDA(mem.alloc(&inv, (size_t)D * Lp));
   MM_CUDA(mem.alloc(&U, (size_t)D * Lp));
-  MM_CUDA(mem.alloc(&keys, (size_t)D * Lp));
+  const long long Lb = (Lp + 31) / 32 * 32;  // blocked arrays: whole 32-window blocks
+  MM_CUDA(mem.alloc(&keys, (size_t)D * Lb));
+  double2 *WU = nullptr, *WI = nullptr;
+  MM_CUDA(mem.alloc(&WU, (size_t)D * Lb));
+  MM_CUDA(mem.alloc(&WI, (size_t)D * Lb));
   MM_CUDA(mem.alloc(&omp, (size_t)dims * L));
   MM_CUDA(mem.alloc(&opi, (size_t)dims * L));
   MM_CUDA(mem.alloc(&odo, (size_t)dims * L));
@@ -1050,7 +1098,7 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
                             cudaMemcpyHostToDevice, st));
 
   MStompParams P{};
-  P.x = x; P.mu = mu; P.inv = inv; P.U = U;
+  P.x = x; P.mu = mu; P.inv = inv; P.U = U; P.WU = WU; P.WI = WI;
   P.n = n; P.ns = ns; P.L = L; P.Lp = Lp; P.khi = L;
   P.keys = keys; P.items = d_items; P.n_items = (long long)items.size();
   P.m = (int)m; P.n_must = n_must; P.D = D; P.imask = imask;
@@ -1060,9 +1108,7 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
     MM_CUDA(mpgpu_internal::series_stats(x + (size_t)q * ns, n, (int)m, mu + (size_t)q * Lp,
                                          inv + (size_t)q * Lp, U + (size_t)q * Lp, nullptr, st));
   const int bs = 256;
-  for (int q = 0; q < D; ++q)
-    k_fill_val<<<(unsigned)((Lp + bs - 1) / bs), bs, 0, st>>>(keys + (size_t)q * Lp, L, Lp, kNoKeyS,
-                                                              kPadKey);
+  k_build_w<<<(unsigned)((Lb * D + bs - 1) / bs), bs, 0, st>>>(U, inv, L, Lp, Lb, D, WU, WI, keys);
   MM_CUDA(cudaGetLastError());
   if (P.n_items > 0) mstomp_launcher(D)(P, st);
   MM_CUDA(cudaGetLastError());

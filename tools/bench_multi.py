@@ -43,9 +43,13 @@ def run(kind, d, n, w, reps=3):
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--case", action="append", default=[],
+                    help="kind,dims,n,window (repeatable); replaces the default list")
     a = ap.parse_args()
     cases = [("simple", 3, 1 << 16, 256), ("mstomp", 3, 1 << 16, 256)]
-    if not a.quick:
+    if a.case:
+        cases = [(c.split(",")[0], *map(int, c.split(",")[1:])) for c in a.case]
+    elif not a.quick:
         cases += [("simple", 1, 1 << 17, 256), ("simple", 12, 1 << 15, 64),
                   ("mstomp", 1, 1 << 17, 256), ("mstomp", 8, 1 << 15, 128)]
     for c in cases:
