@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -116,8 +117,13 @@ struct SimpleParams {
   long long n_items;
   int dims, m;
   long long imask;
+  unsigned long long* stats;  // MPGPU_STATS=1: [steps, slow-path steps, column REDs, row REDs]
 };
 
+// High word of a key. An L1 copy may be stale (RED.MIN lands in L2), which
+// only costs extra slow-path entries (keys never increase); reading at L2
+// (ld.global.cg) measured slower (SiMPle d=1: 11.6 -> 12.3 ms) for the same
+// fire rate.
 __device__ __forceinline__ int key_hi(const long long* k, long long i) {
   return reinterpret_cast<const int*>(k)[2 * i + 1];
 }
@@ -170,70 +176,85 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_t(const SimpleParams
     cnr[d] = S.C.nrm[j];
     cth[d] = key_hi(S.keyC, j);
   }
-  for (int u = 0; u < it.nrows; u += KD) {
-#pragma unroll
-    for (int s = 0; s < KD; ++s) {
-      const long long i = r0 + u + s;
-      const int sin = (s + KD - 1) % KD;
-      {
-        const long long jn = c0 + u + s + KD - 1;  // entering column
-#pragma unroll
-        for (int q = 0; q < DIMS; ++q) {
-          co[sin][q] = jn > 0 ? xc[q * nsC + jn - 1] : 0.0;
-          cn[sin][q] = xc[q * nsC + jn + m - 1];
-        }
-        cnr[sin] = S.C.nrm[jn];
-        cth[sin] = key_hi(S.keyC, jn);
-      }
-      const bool step = (u + s) != 0;  // the seed row takes no update
-      double ro[DIMS], rn[DIMS];
+  // One row-step: the entering column and the row, the recurrence, the squared
+  // distances and the filter; with `slow` the exact key updates run when any
+  // lane passed. Returns this lane's filter result.
+  auto step = [&](const int s, const long long u, const bool slow) -> bool {
+    const long long i = r0 + u + s;
+    const int sin = (s + KD - 1) % KD;
+    {
+      const long long jn = c0 + u + s + KD - 1;  // entering column
 #pragma unroll
       for (int q = 0; q < DIMS; ++q) {
-        ro[q] = step ? xr[q * nsR + i - 1] : 0.0;
-        rn[q] = step ? xr[q * nsR + i + m - 1] : 0.0;
+        co[sin][q] = jn > 0 ? xc[q * nsC + jn - 1] : 0.0;
+        cn[sin][q] = xc[q * nsC + jn + m - 1];
       }
-      const double rnr = S.R.nrm[i];
-      const int rth = key_hi(S.keyR, i);
-      double v[KD];
-      bool fire = false;
-      int hmin = 0x7fffffff;
+      cnr[sin] = S.C.nrm[jn];
+      cth[sin] = key_hi(S.keyC, jn);
+    }
+    const bool upd = (u + s) != 0;  // the seed row takes no update
+    double ro[DIMS], rn[DIMS];
+#pragma unroll
+    for (int q = 0; q < DIMS; ++q) {
+      ro[q] = upd ? xr[q * nsR + i - 1] : 0.0;
+      rn[q] = upd ? xr[q * nsR + i + m - 1] : 0.0;
+    }
+    const double rnr = S.R.nrm[i];
+    const int rth = key_hi(S.keyR, i);
+    double v[KD];
+    bool fire = false;
+    int hmin = 0x7fffffff;
+#pragma unroll
+    for (int d = 0; d < KD; ++d) {
+      const int sl = (s + d) % KD;
+#pragma unroll
+      for (int q = 0; q < DIMS; ++q) {
+        qt[d] = fma(-ro[q], co[sl][q], qt[d]);
+        qt[d] = fma(rn[q], cn[sl][q], qt[d]);
+      }
+      v[d] = fma(-2.0, qt[d], rnr + cnr[sl]);
+      const int h = __double2hiint(v[d]);
+      hmin = min(hmin, h);
+      fire |= h <= cth[sl];
+    }
+    fire |= hmin <= rth;
+    if (slow && __any_sync(0xffffffffu, fire)) {
+      if (P.stats && lane == 0) atomicAdd(&P.stats[1], 1ull);
+      long long best = kNoKeyS;
+      const bool row_ok = i < S.R.L;
 #pragma unroll
       for (int d = 0; d < KD; ++d) {
         const int sl = (s + d) % KD;
-#pragma unroll
-        for (int q = 0; q < DIMS; ++q) {
-          qt[d] = fma(-ro[q], co[sl][q], qt[d]);
-          qt[d] = fma(rn[q], cn[sl][q], qt[d]);
-        }
-        v[d] = fma(-2.0, qt[d], rnr + cnr[sl]);
-        const int h = __double2hiint(v[d]);
-        hmin = min(hmin, h);
-        fire |= h <= cth[sl];
-      }
-      fire |= hmin <= rth;
-      if (__any_sync(0xffffffffu, fire)) {
-        long long best = kNoKeyS;
-        const bool row_ok = i < S.R.L;
-#pragma unroll
-        for (int d = 0; d < KD; ++d) {
-          const int sl = (s + d) % KD;
-          const long long j = c0 + u + s + d;
-          const double vv = fmax(v[d], 0.0);
-          const int h = __double2hiint(vv);
-          if (row_ok && j < S.C.L) {
-            if (h <= cth[sl]) {
-              red_min64(&S.keyC[j], pack_key(vv, i, imask));
-              cth[sl] = min(cth[sl], h);
-            }
-            if (h <= rth) {
-              const long long kr = pack_key(vv, j, imask);
-              best = kr < best ? kr : best;
-            }
+        const long long j = c0 + u + s + d;
+        const double vv = fmax(v[d], 0.0);
+        const int h = __double2hiint(vv);
+        if (row_ok && j < S.C.L) {
+          if (h <= cth[sl]) {
+            if (P.stats) atomicAdd(&P.stats[2], 1ull);
+            red_min64(&S.keyC[j], pack_key(vv, i, imask));
+            cth[sl] = min(cth[sl], h);
+          }
+          if (h <= rth) {
+            const long long kr = pack_key(vv, j, imask);
+            best = kr < best ? kr : best;
           }
         }
-        best = warp_min64(best);
-        if (lane == 0 && best != kNoKeyS) red_min64(&S.keyR[i], best);
       }
+      best = warp_min64(best);
+      if (lane == 0 && best != kNoKeyS) {
+        if (P.stats) atomicAdd(&P.stats[3], 1ull);
+        red_min64(&S.keyR[i], best);
+      }
+    }
+    return fire;
+  };
+  // (Branch-free blocks of KD steps with a replay on fire, as in k_join, were
+  // measured slower here: 11.6 -> 13.0 ms at d = 1, 7.3 -> 8.7 ms at d = 3.)
+  for (int u = 0; u < it.nrows; u += KD) {
+#pragma unroll
+    for (int s = 0; s < KD; ++s) {
+      if (P.stats && lane == 0) atomicAdd(&P.stats[0], 1ull);
+      step(s, u, true);
     }
   }
 }
@@ -271,9 +292,9 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple(const SimpleParams P
     if (ok) {
       kr = pack_key(vv, j, P.imask);
       const long long kc = pack_key(vv, i, P.imask);
-      if (kc < S.keyC[j]) red_min64(&S.keyC[j], kc);
+      if (kc < __ldcg(&S.keyC[j])) red_min64(&S.keyC[j], kc);
     }
-    const long long tr = S.keyR[i];
+    const long long tr = __ldcg(&S.keyR[i]);
     if (__any_sync(0xffffffffu, kr < tr)) {
       const long long b = warp_min64(kr);
       if (lane == 0 && b < tr) red_min64(&S.keyR[i], b);
@@ -487,9 +508,9 @@ __global__ void __launch_bounds__(kMWarps * 32) k_mstomp(const MStompParams P) {
       const long long kr = live ? pack_key(pk, j, P.imask) : kNoKey;
       if (live) {
         const long long kc = pack_key(pk, i, P.imask);
-        if (kc < P.keys[ej + 32 * q]) red_min64(&P.keys[ej + 32 * q], kc);
+        if (kc < __ldcg(&P.keys[ej + 32 * q])) red_min64(&P.keys[ej + 32 * q], kc);
       }
-      const long long tr = P.keys[ei + 32 * q];
+      const long long tr = __ldcg(&P.keys[ei + 32 * q]);
       if (__any_sync(0xffffffffu, kr < tr)) {
         const long long b = warp_min64(kr);
         if (lane == 0 && b < tr) red_min64(&P.keys[ei + 32 * q], b);
@@ -547,7 +568,7 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
     for (int q = 0; q < D; ++q) {
       cu[d][q] = P.WU[e + 32 * q];
       ci[d][q] = P.WI[e + 32 * q];
-      cth[d][q] = khi_[2 * (e + 32 * q)];
+      cth[d][q] = __ldcg(khi_ + 2 * (e + 32 * q));
     }
   }
   for (int u = 0; u < it.nrows; u += KD) {
@@ -561,7 +582,7 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
         for (int q = 0; q < D; ++q) {
           cu[sin][q] = P.WU[e + 32 * q];
           ci[sin][q] = P.WI[e + 32 * q];
-          cth[sin][q] = khi_[2 * (e + 32 * q)];
+          cth[sin][q] = __ldcg(khi_ + 2 * (e + 32 * q));
         }
       }
       const bool step = (u + s) != 0;
@@ -572,7 +593,7 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
       for (int q = 0; q < D; ++q) {
         ru[q] = step ? P.WU[ei + 32 * q] : make_double2(0.0, 0.0);
         ri[q] = P.WI[ei + 32 * q];
-        rth[q] = khi_[2 * (ei + 32 * q)];
+        rth[q] = __ldcg(khi_ + 2 * (ei + 32 * q));
       }
       double pk[KD][D];
       bool fire = false;
@@ -910,7 +931,19 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
   }
   k_fill_val<<<(unsigned)((Lpa + bs - 1) / bs), bs, 0, st>>>(k0, La, Lpa, kNoKeyS, kPadKey);
   k_fill_val<<<(unsigned)((Lpk1 + bs - 1) / bs), bs, 0, st>>>(k1, Lk1, Lpk1, kNoKeyS, kPadKey);
+  unsigned long long* d_stats = nullptr;
+  if (getenv("MPGPU_STATS")) {
+    MM_CUDA(mem.alloc(&d_stats, 4));
+    MM_CUDA(cudaMemsetAsync(d_stats, 0, 32, st));
+    P.stats = d_stats;
+  }
   if (P.n_items > 0) simple_launcher((int)dims)(P, st);
+  if (d_stats) {
+    unsigned long long h[4];
+    MM_CUDA(cudaMemcpyAsync(h, d_stats, 32, cudaMemcpyDeviceToHost, st));
+    MM_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "simple stats: steps %llu slow steps %llu colRED %llu rowRED %llu\n", h[0], h[1], h[2], h[3]);
+  }
   const unsigned fa = (unsigned)((La * 32 + bs - 1) / bs);
   MM_CUDA(cudaGetLastError());
   // outputs land in device scratch, then host

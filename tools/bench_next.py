@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
 """Measurements for the SURVEY §8(f) rows: anytime SCRIMP, the MASS
-distance-profile batch and FLUSS. Each row is timed on the GPU (CUDA events,
+distance-profile batch, FLUSS, mSTOMP and SiMPle. Each row is timed on the GPU (CUDA events,
 inputs resident) against its roofline, next to the CPU oracle on a bounded
 sample.
 
@@ -137,9 +137,65 @@ def fluss_row():
           "cpu_windows_per_s": L / cpu_s, "cpu_threads": 1, "cpu_sample": "oracle numpy restatement, full L"})
 
 
+def _unique_cells(L, zone):
+    r = L - zone - 1
+    return r * (r + 1) // 2 if r > 0 else 0
+
+
+def multivariate_row(kind, d, n, m, ops_per_cell, ops_note):
+    """mSTOMP / SiMPle self-join on d seeded random walks (no BASELINE config
+    names these; SPEC.md:225-243 shapes). GPU: device time of the call's
+    kernels (stats + diagonal kernel + finalize, CUDA events inside the
+    library) and wall time through the API from host buffers. CPU: the
+    oracle's STOMP-order loop over a bounded row sample on all host threads."""
+    g = np.random.default_rng(2018 + d)
+    x = np.cumsum(g.standard_normal((d, n)), axis=1)
+    L = n - m + 1
+    zone = mp.zone_size(m, 0.5)
+    f = (lambda: mp.mstomp(x, m, 0.5, timed=True)) if kind == "mstomp" else \
+        (lambda: mp.simple_join(x, None, m, 0.5, timed=True))
+    f()
+    ks, ws = [], []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        r = f()
+        ws.append(time.perf_counter() - t0)
+        ks.append(r.kernel_ms)
+    k_ms, w_s = float(np.median(ks)), float(np.median(ws))
+    cells = _unique_cells(L, zone)
+    rows = max(THREADS, min(L, int(2e9 / (L * d * (12 if kind == "mstomp" else 4)))))
+    t0 = time.perf_counter()
+    if kind == "mstomp":
+        oracle.mstomp(x, m, 0.5, n_workers=THREADS, row_begin=0, row_end=rows)
+    else:
+        oracle.simple_join(x, None, m, 0.5, n_workers=THREADS, row_begin=0, row_end=rows)
+    cpu_s = time.perf_counter() - t0
+    ach = cells * ops_per_cell / (k_ms * 1e-3)
+    emit({"row": f"8f.4 {'mSTOMP' if kind == 'mstomp' else 'SiMPle'} (d={d})",
+          "workload": f"self-join, {d} random walks, n={n}, m={m}, zone={zone}",
+          "cells": cells, "gpu_ms": k_ms, "cells_per_s": cells / (k_ms * 1e-3),
+          "e2e_ms": 1e3 * w_s, "e2e_cells_per_s": cells / w_s,
+          "roofline": {"bound": "fp64", "achieved": ach / 1e12, "peak": 18.58,
+                       "unit": f"Tops/s ({ops_per_cell} fp64 ops per cell: {ops_note})",
+                       "frac": ach / 18.58e12},
+          "cpu_cells_per_s": cells * rows / L / cpu_s, "cpu_threads": THREADS,
+          "cpu_sample": f"oracle {kind} rows [0,{rows}) of {L}, full rows, unique-cell equivalent"})
+
+
 if __name__ == "__main__":
     oracle.build()
     mp.lib()
-    anytime_scrimp()
-    mass_batch()
-    fluss_row()
+    only = sys.argv[1:]
+    if not only or "scrimp" in only:
+        anytime_scrimp()
+    if not only or "mass" in only:
+        mass_batch()
+    if not only or "fluss" in only:
+        fluss_row()
+    if not only or "multi" in only:
+        for d in (1, 3):
+            multivariate_row("mstomp", d, 1 << 16, 256, 12 * d,
+                             f"per dim 2 recurrence + 2 normalise + 1 distance + 5 sqrt + 2 prefix mean")
+        for d in (1, 3):
+            multivariate_row("simple", d, 1 << 17 if d == 1 else 1 << 16, 256, 2 * d + 2,
+                             "2 per dim recurrence + add + distance")
