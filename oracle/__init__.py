@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
+import sys
 
 import numpy as np
 
@@ -29,7 +30,10 @@ _ref = None
 
 def build() -> None:
     """Compile liboracle.so (and _ref/ when the reference tree is present)."""
-    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    r = subprocess.run(["make", "-s", "-C", _HERE], capture_output=True, text=True)
+    sys.stderr.write(r.stdout + r.stderr)  # keep stdout clean for JSON-line tools
+    if r.returncode != 0:
+        raise RuntimeError("oracle build failed")
 
 
 def _load():

@@ -179,28 +179,42 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_t(const SimpleParams
   // One row-step: the entering column and the row, the recurrence, the squared
   // distances and the filter; with `slow` the exact key updates run when any
   // lane passed. Returns this lane's filter result.
+  // Software pipeline: the entering column and the row of step t + 1 are
+  // loaded while step t computes (the per-step vote would otherwise keep the
+  // scheduler from hoisting them).
+  double pco[DIMS], pcn[DIMS], pro[DIMS], prn[DIMS], pcnr, prnr;
+  int pcth, prth;
+  auto fetch = [&](const long long t) {
+    const long long i = r0 + t, jn = c0 + t + KD - 1;
+#pragma unroll
+    for (int q = 0; q < DIMS; ++q) {
+      pco[q] = jn > 0 ? xc[q * nsC + jn - 1] : 0.0;
+      pcn[q] = xc[q * nsC + jn + m - 1];
+      pro[q] = t > 0 ? xr[q * nsR + i - 1] : 0.0;  // the seed row takes no update
+      prn[q] = t > 0 ? xr[q * nsR + i + m - 1] : 0.0;
+    }
+    pcnr = S.C.nrm[jn];
+    pcth = key_hi(S.keyC, jn);
+    prnr = S.R.nrm[i];
+    prth = key_hi(S.keyR, i);
+  };
+  fetch(0);
   auto step = [&](const int s, const long long u, const bool slow) -> bool {
     const long long i = r0 + u + s;
     const int sin = (s + KD - 1) % KD;
-    {
-      const long long jn = c0 + u + s + KD - 1;  // entering column
-#pragma unroll
-      for (int q = 0; q < DIMS; ++q) {
-        co[sin][q] = jn > 0 ? xc[q * nsC + jn - 1] : 0.0;
-        cn[sin][q] = xc[q * nsC + jn + m - 1];
-      }
-      cnr[sin] = S.C.nrm[jn];
-      cth[sin] = key_hi(S.keyC, jn);
-    }
-    const bool upd = (u + s) != 0;  // the seed row takes no update
     double ro[DIMS], rn[DIMS];
 #pragma unroll
     for (int q = 0; q < DIMS; ++q) {
-      ro[q] = upd ? xr[q * nsR + i - 1] : 0.0;
-      rn[q] = upd ? xr[q * nsR + i + m - 1] : 0.0;
+      co[sin][q] = pco[q];
+      cn[sin][q] = pcn[q];
+      ro[q] = pro[q];
+      rn[q] = prn[q];
     }
-    const double rnr = S.R.nrm[i];
-    const int rth = key_hi(S.keyR, i);
+    cnr[sin] = pcnr;
+    cth[sin] = pcth;
+    const double rnr = prnr;
+    const int rth = prth;
+    fetch(u + s + 1);
     double v[KD];
     bool fire = false;
     int hmin = 0x7fffffff;
@@ -802,7 +816,7 @@ SLaunch simple_launcher(int dims) {
   const int kd = e ? atoi(e) : 0;
   switch (dims) {
     case 1: return kd == 8 ? launch_simple<8, 1> : (kd == 2 ? launch_simple<2, 1> : launch_simple<4, 1>);
-    case 2: return kd == 8 ? launch_simple<8, 2> : (kd == 2 ? launch_simple<2, 2> : launch_simple<4, 2>);
+    case 2: return kd == 8 ? launch_simple<8, 2> : (kd == 4 ? launch_simple<4, 2> : launch_simple<2, 2>);
     case 3: return launch_simple<2, 3>;
     case 4: return launch_simple<2, 4>;
     case 5: return launch_simple<1, 5>;
@@ -816,7 +830,7 @@ SLaunch simple_launcher(int dims) {
 int simple_kd(int dims) {
   const char* e = getenv("MPGPU_SIMPLE_KD");
   const int kd = e ? atoi(e) : 0;
-  if (dims <= 2) return (kd == 8 || kd == 2) ? kd : 4;
+  if (dims <= 2) return (kd == 8 || kd == 2 || kd == 4) ? kd : (dims == 1 ? 4 : 2);
   if (dims <= 4) return 2;
   return 1;
 }
