@@ -11,6 +11,8 @@
  *   mpgpu_distance_profiles        <- mprof::mass_distance_profile (distance.hpp:26-33), batched
  *   mpgpu_fluss / mpgpu_extract    <- fluss_arc_count / fluss_cac / fluss_extract / find_discord
  *                                     (discovery.hpp:61-79)
+ *   mpgpu_mstomp                   <- mprof::mstomp (profile.hpp:91-94)
+ *   mpgpu_simple_join              <- mprof::simple_join (profile.hpp:96-100)
  *   mpgpu_rolling_stats            <- mprof::rolling_mean_std (rolling.hpp:25-29)
  *                                     + is_flat_std (rolling.hpp:21-23)
  *   mpgpu_plan_*                   <- the stomp worker-chunk contract

@@ -71,15 +71,17 @@ __device__ __forceinline__ long long warp_min64(long long v) {
   return v;
 }
 
-// sqrt for the search (s >= 0): MUFU reciprocal square root + one Newton step
-// (relative error ~1e-13; the reported values are recomputed exactly).
+// sqrt for the search (s >= 0) as s * rsqrt(s): rsqrt.approx.ftz.f64 is the
+// bare MUFU.RSQ64H (relative error 2^-20) and one Newton step brings it to
+// 1.3e-12 (tools/microbench/rsqrt_accuracy.cu); 5 fp64 ops in all. The
+// non-ftz rsqrt.approx.f64 is already refined by ptxas (5 ops and a slow-path
+// branch), and sqrt() adds a further refinement on top.
 __device__ __forceinline__ double sqrt_search(double s) {
-  const double s2 = s + 1e-300;  // s >= 0: keeps rsqrt finite at 0
+  const double s2 = s + 1e-300;  // keeps rsqrt finite at 0
   double y;
-  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(s2));
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s2));
   const double h = 0.5 * s2;
-  const double e = fma(-h * y, y, 0.5);
-  y = fma(y, e, y);
+  y = fma(y, fma(-h * y, y, 0.5), y);
   return s * y;
 }
 
