@@ -365,11 +365,6 @@ __global__ void k_simple_finalize(const double* X, long long nx, long long LX, c
   }
 }
 
-__global__ void k_fill(long long* k, long long len) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < len) k[i] = kNoKey;
-}
-
 __global__ void k_fill_val(long long* k, long long len, long long total, long long v, long long pad) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < total) k[i] = i < len ? v : pad;
@@ -748,53 +743,57 @@ int ceil_log2ll(long long v) {
   return b;
 }
 
-// Bands of 32 diagonals in [klo, khi) x row segments of `seg` rows, for
-// cells (i, i + k) with i < min(LR, LC - k). Largest items first.
-void build_mitems(std::vector<MItem>& out, int pass, long long klo, long long khi, long long LR,
-                  long long LC, long long seg) {
-  for (long long kb = klo; kb < khi; kb += 32) {
-    const long long rows = std::min(LR, LC - kb);
-    for (long long r0 = 0; r0 < rows; r0 += seg)
-      out.push_back(MItem{kb, r0, (int)std::min(seg, rows - r0), pass});
-  }
-}
-
 void sort_mitems(std::vector<MItem>& v) {
   std::stable_sort(v.begin(), v.end(), [](const MItem& a, const MItem& b) { return a.nrows > b.nrows; });
 }
 
-// segment rows: long enough to amortise the O(m) seed, short enough to fill the GPU
-long long seg_rows(long long m, long long L) {
-  long long s = std::max<long long>(512, 4 * m);
-  return std::min(s, std::max<long long>(L, 1));
-}
-
-struct DevMem {
-  std::vector<void*> p;
-  ~DevMem() {
-    for (void* q : p) cudaFree(q);
-  }
+// Per-(device, entry point) scratch reused across calls: the i-th allocation
+// of a call reuses the i-th block when it is large enough (calls are
+// serialised, and every entry point allocates in a fixed order), so a repeated
+// join pays no cudaMalloc / cudaFree. The stream and timing events persist too.
+struct Arena {
+  std::vector<void*> blk;
+  std::vector<size_t> cap;
+  size_t next = 0;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ea = nullptr, eb = nullptr;
   template <class T>
   cudaError_t alloc(T** out, size_t count) {
-    void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, sizeof(T) * std::max<size_t>(count, 1));
-    if (e == cudaSuccess) {
-      p.push_back(q);
-      *out = (T*)q;
+    const size_t bytes = sizeof(T) * std::max<size_t>(count, 1);
+    if (next == blk.size()) {
+      blk.push_back(nullptr);
+      cap.push_back(0);
     }
-    return e;
+    if (cap[next] < bytes) {
+      if (blk[next]) cudaFree(blk[next]);
+      blk[next] = nullptr;
+      cap[next] = 0;
+      const cudaError_t e = cudaMalloc(&blk[next], bytes);
+      if (e != cudaSuccess) return e;
+      cap[next] = bytes;
+    }
+    *out = (T*)blk[next++];
+    return cudaSuccess;
   }
 };
 
-struct Timer {
-  cudaEvent_t a = nullptr, b = nullptr;
-  ~Timer() {
-    if (a) cudaEventDestroy(a);
-    if (b) cudaEventDestroy(b);
-  }
-};
+std::vector<std::unique_ptr<Arena>> g_arenas;  // index: device * 2 + kind
 
-std::mutex g_multi_mu;  // calls are serialised (scratch is per call)
+// The arena of (device, kind), its stream and events created on first use.
+mpgpu_status arena_for(int device, int kind, Arena** out) {
+  const size_t slot = (size_t)device * 2 + (size_t)kind;
+  if (g_arenas.size() <= slot) g_arenas.resize(slot + 1);
+  if (!g_arenas[slot]) g_arenas[slot].reset(new Arena());
+  Arena* A = g_arenas[slot].get();
+  if (!A->st) MM_CUDA(cudaStreamCreateWithFlags(&A->st, cudaStreamNonBlocking));
+  if (!A->ea) MM_CUDA(cudaEventCreate(&A->ea));
+  if (!A->eb) MM_CUDA(cudaEventCreate(&A->eb));
+  A->next = 0;
+  *out = A;
+  return MPGPU_OK;
+}
+
+std::mutex g_multi_mu;  // calls are serialised (the arenas are shared)
 
 }  // namespace
 
@@ -851,15 +850,10 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
   if (self && A->zone < 0) return set_error(MPGPU_EPARAM, "negative exclusion zone");
   std::lock_guard<std::mutex> lk(g_multi_mu);
   MM_CUDA(cudaSetDevice(A->device));
-  cudaStream_t st = nullptr;
-  MM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
-  } sg{st};
-  Timer tm;
-  MM_CUDA(cudaEventCreate(&tm.a));
-  MM_CUDA(cudaEventCreate(&tm.b));
+  Arena* ar = nullptr;
+  if (mpgpu_status e = arena_for(A->device, 0, &ar); e != MPGPU_OK) return e;
+  cudaStream_t st = ar->st;
+  Arena& mem = *ar;
 
   const long long na = A->n_a, nb = self ? na : A->n_b;
   const long long La = na - m + 1, Lb = nb - m + 1;
@@ -867,7 +861,6 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
   const long long pad = kSimplePad;
   const long long nsa = na + pad + m, nsb = nb + pad + m;   // padded strides
   const long long Lpa = La + pad, Lpb = Lb + pad;
-  DevMem mem;
   double *xa, *xb = nullptr, *xca, *xcb = nullptr, *nra, *nrb = nullptr, *shift;
   long long *k0, *k1;
   MM_CUDA(mem.alloc(&xa, dims * na));
@@ -937,7 +930,7 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
   P.items = d_items;
   P.n_items = (long long)items.size();
 
-  MM_CUDA(cudaEventRecord(tm.a, st));
+  MM_CUDA(cudaEventRecord(ar->ea, st));
   const int bs = 256;
   k_center<<<(unsigned)((dims * nsa + bs - 1) / bs), bs, 0, st>>>(xa, na, nsa, (int)dims, shift, xca);
   k_raw_energy<<<(unsigned)((Lpa + bs - 1) / bs), bs, 0, st>>>(xca, nsa, La, Lpa, (int)dims, (int)m, nra);
@@ -981,7 +974,7 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
         xb, nb, Lb, xa, na, k1, nullptr, (int)dims, (int)m, imask, omp_b, opi_b, nullptr, nullptr);
   }
   MM_CUDA(cudaGetLastError());
-  MM_CUDA(cudaEventRecord(tm.b, st));
+  MM_CUDA(cudaEventRecord(ar->eb, st));
   if (A->mp_a) MM_CUDA(cudaMemcpyAsync(A->mp_a, omp_a, sizeof(double) * La, cudaMemcpyDeviceToHost, st));
   if (A->pi_a) MM_CUDA(cudaMemcpyAsync(A->pi_a, opi_a, sizeof(long long) * La, cudaMemcpyDeviceToHost, st));
   if (self && A->left_a)
@@ -995,7 +988,7 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
   MM_CUDA(cudaStreamSynchronize(st));
   if (A->kernel_ms) {
     float ms = 0.f;
-    MM_CUDA(cudaEventElapsedTime(&ms, tm.a, tm.b));
+    MM_CUDA(cudaEventElapsedTime(&ms, ar->ea, ar->eb));
     *A->kernel_ms = ms;
   }
   return MPGPU_OK;
@@ -1087,20 +1080,14 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
   const int n_must = (int)A->n_must;
   std::lock_guard<std::mutex> lk(g_multi_mu);
   MM_CUDA(cudaSetDevice(A->device));
-  cudaStream_t st = nullptr;
-  MM_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  struct StreamGuard {
-    cudaStream_t s;
-    ~StreamGuard() { cudaStreamDestroy(s); }
-  } sg{st};
-  Timer tm;
-  MM_CUDA(cudaEventCreate(&tm.a));
-  MM_CUDA(cudaEventCreate(&tm.b));
+  Arena* ar = nullptr;
+  if (mpgpu_status e = arena_for(A->device, 1, &ar); e != MPGPU_OK) return e;
+  cudaStream_t st = ar->st;
+  Arena& mem = *ar;
 
   const long long L = n - m + 1, pad = mpgpu_internal::stats_pad(), Lp = L + pad;
   const long long ns = n + pad;
   if (L >= (1LL << 31)) return set_error(MPGPU_EUNSUPPORTED, "profile longer than 2^31");
-  DevMem mem;
   double *x, *mu, *inv, *omp;
   double2* U;
   long long *keys, *opi, *odo;
@@ -1152,7 +1139,7 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
   P.keys = keys; P.items = d_items; P.n_items = (long long)items.size();
   P.m = (int)m; P.n_must = n_must; P.D = D; P.imask = imask;
 
-  MM_CUDA(cudaEventRecord(tm.a, st));
+  MM_CUDA(cudaEventRecord(ar->ea, st));
   for (int q = 0; q < D; ++q)
     MM_CUDA(mpgpu_internal::series_stats(x + (size_t)q * ns, n, (int)m, mu + (size_t)q * Lp,
                                          inv + (size_t)q * Lp, U + (size_t)q * Lp, nullptr, st));
@@ -1165,7 +1152,7 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
   k_mstomp_finalize<<<(unsigned)((outs * 32 + bs - 1) / bs), bs, 0, st>>>(P, D, (int)dims, dperm,
                                                                          omp, opi, odo);
   MM_CUDA(cudaGetLastError());
-  MM_CUDA(cudaEventRecord(tm.b, st));
+  MM_CUDA(cudaEventRecord(ar->eb, st));
   if (A->mp) MM_CUDA(cudaMemcpyAsync(A->mp, omp, sizeof(double) * outs, cudaMemcpyDeviceToHost, st));
   if (A->pi) MM_CUDA(cudaMemcpyAsync(A->pi, opi, sizeof(long long) * outs, cudaMemcpyDeviceToHost, st));
   if (A->dim_order)
@@ -1173,7 +1160,7 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
   MM_CUDA(cudaStreamSynchronize(st));
   if (A->kernel_ms) {
     float ms = 0.f;
-    MM_CUDA(cudaEventElapsedTime(&ms, tm.a, tm.b));
+    MM_CUDA(cudaEventElapsedTime(&ms, ar->ea, ar->eb));
     *A->kernel_ms = ms;
   }
   return MPGPU_OK;
