@@ -184,3 +184,42 @@ def test_multivariate_errors(mp):
         mp.simple_join(x, None, 65)                                # window > n
     with pytest.raises(mp.ParameterError):
         mp.MultiTimeSeries([x[0], x[1][:50]])                      # unequal lengths
+
+
+def test_multivariate_edge_shapes(mp, oracle_lib):
+    """L = 1, zone >= L - 1 (nothing admissible), w = 4, constant dims, AB with
+    L_B = 1: +inf / -1 where every candidate is excluded."""
+    g = np.random.default_rng(61)
+    x = _walk(g, 3, 40)
+    # L = 1: no partner at all
+    s1 = mp.simple_join(x[:, :8], None, 8, 0.5)
+    assert np.isinf(s1.values).all() and (s1.index == -1).all()
+    m1 = mp.mstomp(x[:, :8], 8, 0.5)
+    assert np.isinf(m1.values).all() and (m1.index == -1).all() and (m1.dim_order == -1).all()
+    # zone covers everything: ez = 10 -> zone = 80 > L
+    s2 = mp.simple_join(x, None, 8, 10.0)
+    assert np.isinf(s2.values).all() and (s2.left_index == -1).all() and (s2.right_index == -1).all()
+    m2 = mp.mstomp(x, 8, 10.0)
+    assert np.isinf(m2.values).all()
+    # minimum window, partially constant dims, against the oracle
+    y = _walk(g, 3, 300)
+    y[1] = 2.5                                   # a constant dimension
+    y[0, 100:160] = -1.0
+    _check_simple_self(mp, oracle_lib, y, 4, 0.5, "w=4 flats")
+    _check_mstomp(mp, oracle_lib, y, 4, label="w=4 flats")
+    # AB with a one-window B
+    a, b = _walk(g, 2, 200), _walk(g, 2, 16)
+    pa, pb = mp.simple_join(a, b, 16, want_b=True)
+    ra = oracle_lib.simple_join(a, b, 16)
+    assert close(pa.values, ra[0])[0] and (pa.index == 0).all()
+    rb = oracle_lib.simple_join(b, a, 16)
+    assert close(pb.values, rb[0])[0]
+
+
+def test_mstomp_constant_series(mp, oracle_lib):
+    """Every window flat in every dim: all distances 0 (flat-vs-flat), values 0."""
+    x = np.ones((2, 64)) * np.array([[3.0], [-1.0]])
+    r = mp.mstomp(x, 8, 0.5)
+    ref = oracle_lib.mstomp(x, 8, 0.5)
+    assert np.all(r.values == 0.0) and np.all(ref[0] == 0.0)
+    assert np.array_equal(r.index, ref[1])           # smallest admissible partner, as the oracle
