@@ -275,6 +275,118 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_t(const SimpleParams
   }
 }
 
+// Any dimension count, dims outermost: a tile of T row-steps x KD diagonals
+// per lane accumulates the QT increments of every (step, diagonal) dimension by
+// dimension (2 DFMA each), so one dimension's T row values and T + KD - 1
+// column values are live at a time whatever the dimension count; the cells
+// are then evaluated step by step (running QT, squared distance, high-word
+// filter, exact updates on a pass) as in k_simple_t.
+template <int KD, int T>
+__global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_dt(const SimpleParams P) {
+  const long long wid = (long long)blockIdx.x * kMWarps + (threadIdx.x >> 5);
+  if (wid >= P.n_items) return;
+  const int lane = threadIdx.x & 31;
+  const MItem it = P.items[wid];
+  const SimplePass& S = P.pass[it.pass];
+  const double* __restrict__ xr = S.R.xc;
+  const double* __restrict__ xc = S.C.xc;
+  const long long nsR = S.R.ns, nsC = S.C.ns;
+  const int m = P.m, dims = P.dims;
+  const long long r0 = it.r0;
+  const long long c0 = r0 + it.kb + (long long)lane * KD;
+  const long long imask = P.imask;
+
+  double qt[KD];
+#pragma unroll
+  for (int d = 0; d < KD; ++d) qt[d] = 0.0;
+  for (int q = 0; q < dims; ++q) {
+    const double* a = xr + q * nsR + r0;
+    const double* c = xc + q * nsC + c0;
+    for (int t = 0; t < m; ++t) {
+      const double av = a[t];
+#pragma unroll
+      for (int d = 0; d < KD; ++d) qt[d] = fma(av, c[t + d], qt[d]);
+    }
+  }
+  constexpr int E = T + KD - 1;  // columns a tile touches per lane
+  for (int u = 0; u < it.nrows; u += T) {
+    double dl[T][KD];
+#pragma unroll
+    for (int s = 0; s < T; ++s)
+#pragma unroll
+      for (int d = 0; d < KD; ++d) dl[s][d] = 0.0;
+    const long long ib = r0 + u, jb = c0 + u;
+    for (int q = 0; q < dims; ++q) {
+      const double* rq = xr + q * nsR + ib;
+      const double* cq = xc + q * nsC + jb;
+      double ro[T], rn[T], co[E], cn[E];
+#pragma unroll
+      for (int s = 0; s < T; ++s) {
+        const bool upd = (u + s) != 0;  // the seed row takes no update
+        ro[s] = upd ? rq[s - 1] : 0.0;
+        rn[s] = upd ? rq[s + m - 1] : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        co[e] = (jb + e) > 0 ? cq[e - 1] : 0.0;
+        cn[e] = cq[e + m - 1];
+      }
+#pragma unroll
+      for (int s = 0; s < T; ++s)
+#pragma unroll
+        for (int d = 0; d < KD; ++d)
+          dl[s][d] = fma(rn[s], cn[s + d], fma(-ro[s], co[s + d], dl[s][d]));
+    }
+    double cnr[E];
+    int cth[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      cnr[e] = S.C.nrm[jb + e];
+      cth[e] = key_hi(S.keyC, jb + e);
+    }
+#pragma unroll
+    for (int s = 0; s < T; ++s) {
+      const long long i = ib + s;
+      const double rnr = S.R.nrm[i];
+      const int rth = key_hi(S.keyR, i);
+      double v[KD];
+      bool fire = false;
+      int hmin = 0x7fffffff;
+#pragma unroll
+      for (int d = 0; d < KD; ++d) {
+        qt[d] += dl[s][d];
+        v[d] = fma(-2.0, qt[d], rnr + cnr[s + d]);
+        const int h = __double2hiint(v[d]);
+        hmin = min(hmin, h);
+        fire |= h <= cth[s + d];
+      }
+      fire |= hmin <= rth;
+      if (__any_sync(0xffffffffu, fire)) {
+        long long best = kNoKeyS;
+        const bool row_ok = i < S.R.L;
+#pragma unroll
+        for (int d = 0; d < KD; ++d) {
+          const long long j = jb + s + d;
+          const double vv = fmax(v[d], 0.0);
+          const int h = __double2hiint(vv);
+          if (row_ok && j < S.C.L) {
+            if (h <= cth[s + d]) {
+              red_min64(&S.keyC[j], pack_key(vv, i, imask));
+              cth[s + d] = min(cth[s + d], h);
+            }
+            if (h <= rth) {
+              const long long kr = pack_key(vv, j, imask);
+              best = kr < best ? kr : best;
+            }
+          }
+        }
+        best = warp_min64(best);
+        if (lane == 0 && best != kNoKeyS) red_min64(&S.keyR[i], best);
+      }
+    }
+  }
+}
+
 // Any dimension count: one diagonal per lane, column data read per step.
 __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple(const SimpleParams P) {
   const long long wid = (long long)blockIdx.x * kMWarps + (threadIdx.x >> 5);
@@ -804,36 +916,62 @@ void launch_simple(const SimpleParams& P, cudaStream_t st) {
   k_simple_t<KD, DIMS><<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
 }
 
+template <int KD, int T>
+void launch_simple_dt(const SimpleParams& P, cudaStream_t st) {
+  k_simple_dt<KD, T><<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
+}
+
 void launch_simple_generic(const SimpleParams& P, cudaStream_t st) {
   k_simple<<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
 }
 
 using SLaunch = void (*)(const SimpleParams&, cudaStream_t);
 
+bool simple_tiled(long long dims) {
+  const char* t = getenv("MPGPU_SIMPLE_TILED");  // experiments: 1 forces k_simple_dt, 0 forbids it
+  if (t) return atoi(t) != 0;
+  return dims > 3;  // measured crossover: the register window wins for d <= 3
+}
+
 SLaunch simple_launcher(int dims) {
   // diagonals per lane by register budget (128 at 2 CTAs/SM); MPGPU_SIMPLE_KD
   // overrides it for dims 1-2 (experiments)
   const char* e = getenv("MPGPU_SIMPLE_KD");
   const int kd = e ? atoi(e) : 0;
+  if (simple_tiled(dims)) dims = 99;  // -> the tiled kernels below
   switch (dims) {
     case 1: return kd == 8 ? launch_simple<8, 1> : (kd == 2 ? launch_simple<2, 1> : launch_simple<4, 1>);
     case 2: return kd == 8 ? launch_simple<8, 2> : (kd == 4 ? launch_simple<4, 2> : launch_simple<2, 2>);
     case 3: return launch_simple<2, 3>;
-    case 4: return launch_simple<2, 4>;
-    case 5: return launch_simple<1, 5>;
-    case 6: return launch_simple<1, 6>;
-    case 7: return launch_simple<1, 7>;
-    case 8: return launch_simple<1, 8>;
-    default: return launch_simple_generic;
+    default: break;
   }
+  const char* t = getenv("MPGPU_SIMPLE_DT");
+  const std::string v = t ? t : "";
+  if (v == "2x4") return launch_simple_dt<2, 4>;
+  if (v == "2x8") return launch_simple_dt<2, 8>;
+  if (v == "4x8") return launch_simple_dt<4, 8>;
+  if (v == "1x1") return launch_simple_generic;
+  if (v == "4x4") return launch_simple_dt<4, 4>;
+  return launch_simple_dt<4, 8>;
+}
+
+// dims > 8: rows per item must be a multiple of the tile's T and bands are 32 KD wide
+int simple_dt_kd() {
+  const char* t = getenv("MPGPU_SIMPLE_DT");
+  const std::string v = t ? t : "";
+  return (v == "2x4" || v == "2x8") ? 2 : (v == "1x1" ? 1 : 4);
+}
+int simple_dt_t() {
+  const char* t = getenv("MPGPU_SIMPLE_DT");
+  const std::string v = t ? t : "";
+  return (v == "2x4" || v == "4x4") ? 4 : (v == "1x1" ? 1 : 8);
 }
 
 int simple_kd(int dims) {
   const char* e = getenv("MPGPU_SIMPLE_KD");
   const int kd = e ? atoi(e) : 0;
   if (dims <= 2) return (kd == 8 || kd == 2 || kd == 4) ? kd : (dims == 1 ? 4 : 2);
-  if (dims <= 4) return 2;
-  return 1;
+  return 2;
 }
 
 }  // namespace
@@ -891,9 +1029,11 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
   const long long imask = (1LL << index_bits) - 1;
 
   // compile-time dims / diagonals per lane up to 16 dims, else the generic kernel
-  const int KD = simple_kd((int)dims);
-  const bool generic = dims > 8;
-  const int band = generic ? 32 : 32 * KD;
+  const bool tiled = simple_tiled(dims);  // k_simple_dt (dims outermost)
+  const int KD = tiled ? simple_dt_kd() : simple_kd((int)dims);
+  const int TR = tiled ? simple_dt_t() : KD;  // rows per item: a multiple of this
+  const bool generic = tiled && KD == 1 && TR == 1;
+  const int band = 32 * KD;
   std::vector<MItem> items;
   const long long seg = std::max<long long>(1024, 8 * m);
   auto build = [&](int pass, long long klo, long long khi, long long LR, long long LC) {
@@ -901,7 +1041,7 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
       const long long rows = std::min(LR, LC - kb);
       for (long long r0 = 0; r0 < rows; r0 += seg) {
         long long nr = std::min(seg, rows - r0);
-        if (!generic) nr = (nr + KD - 1) / KD * KD;  // whole KD-step groups (padding covers the tail)
+        if (!generic) nr = (nr + TR - 1) / TR * TR;  // whole step groups (padding covers the tail)
         items.push_back(MItem{kb, r0, (int)nr, pass});
       }
     }

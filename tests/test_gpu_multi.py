@@ -223,3 +223,16 @@ def test_mstomp_constant_series(mp, oracle_lib):
     ref = oracle_lib.mstomp(x, 8, 0.5)
     assert np.all(r.values == 0.0) and np.all(ref[0] == 0.0)
     assert np.array_equal(r.index, ref[1])           # smallest admissible partner, as the oracle
+
+
+def test_simple_many_dims(mp, oracle_lib):
+    """d > 8 runs the dims-outermost tiled kernel (k_simple_dt)."""
+    g = np.random.default_rng(71)
+    _check_simple_self(mp, oracle_lib, _walk(g, 10, 700), 20, 0.5, "d=10")
+    _check_simple_self(mp, oracle_lib, g.uniform(0, 1, (12, 900)), 16, 0.25, "d=12 uniform")
+    a, b = _walk(g, 9, 500), _walk(g, 9, 300)
+    pa, pb = mp.simple_join(a, b, 24, want_b=True)
+    for got, ref, x, y in ((pa, oracle_lib.simple_join(a, b, 24), a, b),
+                           (pb, oracle_lib.simple_join(b, a, 24), b, a)):
+        assert close(got.values, ref[0])[0]
+        assert not raw_index_mismatches(got.index, ref[1], np.arange(got.values.size), x, y, 24)
