@@ -196,6 +196,5 @@ if __name__ == "__main__":
         for d in (1, 3):
             multivariate_row("mstomp", d, 1 << 16, 256, 12 * d,
                              f"per dim 2 recurrence + 2 normalise + 1 distance + 5 sqrt + 2 prefix mean")
-        for d in (1, 3):
-            multivariate_row("simple", d, 1 << 17 if d == 1 else 1 << 16, 256, 2 * d + 2,
-                             "2 per dim recurrence + add + distance")
+        for d, n, m in ((1, 1 << 17, 256), (3, 1 << 16, 256), (12, 1 << 15, 64)):
+            multivariate_row("simple", d, n, m, 2 * d + 2, "2 per dim recurrence + add + distance")
