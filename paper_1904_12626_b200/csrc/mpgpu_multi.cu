@@ -106,6 +106,8 @@ struct RawSeries {
   const double* xc;   // dims x ns (stride), centred per dim (shared shift), zero padded
   const double* nrm;  // L + pad: summed centred window energies, +inf in the padding
   long long n, ns, L;
+  const double2* V;   // dims x Lp: V[q][j] = {xc_q[j-1], xc_q[j+m-1]} (ring kernel), zero padded
+  long long Lp;
 };
 struct SimplePass {
   RawSeries R, C;
@@ -273,6 +275,251 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_t(const SimpleParams
       step(s, u, true);
     }
   }
+}
+
+// ---- SiMPle on a shared-memory ring (k_join's data path) ---------------------
+// Same cells, filter and key updates as k_simple_t, but every operand comes
+// from a per-warp shared-memory ring filled by cp.async one tile ahead: rows
+// of tile t+1 (kSH rows) and the kSH columns entering the band while tile t
+// computes, so the row-step loop never waits on L1/L2. A column record is
+// DIMS planes of V = {x[j-1], x[j+m-1]} plus {energy, key}, each plane
+// blocked-transposed so the 32 lanes' entering columns are 32 consecutive
+// 16-byte slots (conflict-free LDS.128). Rows are broadcast loads.
+constexpr int kSH = 32;  // rows per tile
+
+template <int KD, int DIMS>
+struct SRing {
+  static constexpr int kWs = 32 * KD;                                   // diagonals per band
+  static constexpr int R = ((kWs + 2 * kSH + KD - 1) / KD) * KD;        // ring slots
+  static constexpr int NB = R / KD;
+  static constexpr int kPlanes = DIMS + 1;
+  static constexpr int kRowPlane = kSH + 1;
+  static constexpr int kPerWarp = kPlanes * R + 2 * kPlanes * kRowPlane;  // double2 per warp
+  static constexpr size_t kSmem = sizeof(double2) * kPerWarp * kMWarps;
+  // rows padded to whole tiles and the band's last columns stay inside the padding
+  static_assert(kWs + kSH <= kSimplePad, "padding too short for the ring kernel");
+};
+
+__device__ __forceinline__ unsigned sm_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sm_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cpa8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sm_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <int KD, int DIMS, bool BLK>
+__global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_r(const SimpleParams P) {
+  using G = SRing<KD, DIMS>;
+  constexpr int R = G::R, NB = G::NB, NP = G::kPlanes, RP = G::kRowPlane, kWs = G::kWs;
+  extern __shared__ double2 sring[];
+  double2* const ring = sring + (threadIdx.x >> 5) * G::kPerWarp;  // plane e at ring + e R
+  double2* const rows = ring + NP * R;                              // (buf NP + e) RP + h
+  const long long wid = (long long)blockIdx.x * kMWarps + (threadIdx.x >> 5);
+  if (wid >= P.n_items) return;
+  const int lane = threadIdx.x & 31;
+  const MItem it = P.items[wid];
+  const SimplePass& S = P.pass[it.pass];
+  const int m = P.m;
+  const long long r0 = it.r0;
+  const long long cw = r0 + it.kb;             // column of (lane 0, d = 0) at row r0
+  const long long c0 = cw + (long long)lane * KD;
+  const long long imask = P.imask;
+  const long long LpR = S.R.Lp, LpC = S.C.Lp;
+  const int nT = it.nrows / kSH;
+
+  auto raddr = [](int x) {  // x: column offset from cw (< 2^31; 32-bit slot math)
+    const int p = x % R;
+    return (p % KD) * NB + p / KD;
+  };
+  auto fetch_col = [&](int x) {
+    const long long j = cw + x;
+    const int a = raddr(x);
+#pragma unroll
+    for (int q = 0; q < DIMS; ++q) cpa16(&ring[q * R + a], &S.C.V[q * LpC + j]);
+    cpa8(&ring[DIMS * R + a].x, &S.C.nrm[j]);
+    cpa8(&ring[DIMS * R + a].y, &S.keyC[j]);
+  };
+  auto fetch_row = [&](int buf, int h, long long i) {
+#pragma unroll
+    for (int q = 0; q < DIMS; ++q) cpa16(&rows[(buf * NP + q) * RP + h], &S.R.V[q * LpR + i]);
+    cpa8(&rows[(buf * NP + DIMS) * RP + h].x, &S.R.nrm[i]);
+    cpa8(&rows[(buf * NP + DIMS) * RP + h].y, &S.keyR[i]);
+  };
+
+  // tile 0 in flight while the seeds are computed
+  fetch_row(0, lane, r0 + lane);
+  for (int x = lane; x < kSH + kWs - 1; x += 32) fetch_col(x);
+
+  // seeds: QT(r0, c0 + d) by direct dot products over all dims
+  double qt[KD];
+#pragma unroll
+  for (int d = 0; d < KD; ++d) qt[d] = 0.0;
+#pragma unroll
+  for (int q = 0; q < DIMS; ++q) {
+    const double* a = S.R.xc + q * S.R.ns + r0;
+    const double* c = S.C.xc + q * S.C.ns + c0;
+    for (int t = 0; t < m; ++t) {
+      const double av = a[t];
+#pragma unroll
+      for (int d = 0; d < KD; ++d) qt[d] = fma(av, c[t + d], qt[d]);
+    }
+  }
+  cpa_wait();
+  __syncwarp();
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < DIMS; ++q) rows[q * RP] = make_double2(0.0, 0.0);  // the seed row takes no update
+  }
+  __syncwarp();
+
+  double2 cv[KD][DIMS];
+  double ce[KD];
+  int cth[KD];
+#pragma unroll
+  for (int d = 0; d < KD - 1; ++d) {  // slots 0..KD-2: columns lane KD + d
+    const int a = d * NB + lane;
+#pragma unroll
+    for (int q = 0; q < DIMS; ++q) cv[d][q] = ring[q * R + a];
+    const double2 e = ring[DIMS * R + a];
+    ce[d] = e.x;
+    cth[d] = __double2hiint(e.y);
+  }
+
+  for (int t = 0; t < nT; ++t) {
+    const int buf = t & 1;
+    const int ts = t * kSH;
+    if (t + 1 < nT) {
+      fetch_row(buf ^ 1, lane, r0 + ts + kSH + lane);
+      fetch_col(ts + kSH + kWs - 1 + lane);
+    }
+    int b0 = (int)((ts / KD + lane) % NB), b1 = 0;
+    // One row-step: the entering column and the row from the ring, the
+    // recurrence, the squared distances and the filter. Without `slow` it only
+    // reports whether this lane passed; with it, a step in which any lane
+    // passed runs the exact key updates.
+    auto step = [&](const int s, const int u, const bool slow) -> bool {
+      const int h = u + s;
+      const int sin = (s + KD - 1) % KD;
+      {
+        const int a = sin * NB + (s == 0 ? b0 : b1);
+#pragma unroll
+        for (int q = 0; q < DIMS; ++q) cv[sin][q] = ring[q * R + a];
+        const double2 e = ring[DIMS * R + a];
+        ce[sin] = e.x;
+        cth[sin] = __double2hiint(e.y);
+      }
+      double2 rv[DIMS];
+#pragma unroll
+      for (int q = 0; q < DIMS; ++q) rv[q] = rows[(buf * NP + q) * RP + h];
+      const double2 re = rows[(buf * NP + DIMS) * RP + h];
+      const int rth = __double2hiint(re.y);
+      double v[KD];
+      bool fire = false;
+      int hmin = 0x7fffffff;
+#pragma unroll
+      for (int d = 0; d < KD; ++d) {
+        const int sl = (s + d) % KD;
+#pragma unroll
+        for (int q = 0; q < DIMS; ++q) {
+          qt[d] = fma(-rv[q].x, cv[sl][q].x, qt[d]);
+          qt[d] = fma(rv[q].y, cv[sl][q].y, qt[d]);
+        }
+        v[d] = fma(-2.0, qt[d], re.x + ce[sl]);
+        const int hv = __double2hiint(v[d]);
+        hmin = min(hmin, hv);
+        fire |= hv <= cth[sl];
+      }
+      fire |= hmin <= rth;
+      if (slow && __any_sync(0xffffffffu, fire)) {
+        if (P.stats && lane == 0) atomicAdd(&P.stats[1], 1ull);
+        const int rho = ts + h;
+        const long long i = r0 + rho;
+        long long best = kNoKeyS;
+        const bool row_ok = i < S.R.L;
+#pragma unroll
+        for (int d = 0; d < KD; ++d) {
+          const int sl = (s + d) % KD;
+          const long long j = c0 + rho + d;
+          const double vv = fmax(v[d], 0.0);
+          const int hv = __double2hiint(vv);
+          if (row_ok && j < S.C.L) {
+            if (hv <= cth[sl]) {
+              if (P.stats) atomicAdd(&P.stats[2], 1ull);
+              const long long kc = pack_key(vv, i, imask);
+              red_min64(&S.keyC[j], kc);
+              cth[sl] = min(cth[sl], hv);
+              // the lane that takes this column next reads the lowered key
+              double2& e = ring[DIMS * R + raddr(rho + lane * KD + d)];
+              if (kc < __double_as_longlong(e.y)) e.y = __longlong_as_double(kc);
+            }
+            if (hv <= rth) {
+              const long long kr = pack_key(vv, j, imask);
+              best = kr < best ? kr : best;
+            }
+          }
+        }
+        best = warp_min64(best);
+        if (lane == 0 && best != kNoKeyS) {
+          if (P.stats) atomicAdd(&P.stats[3], 1ull);
+          red_min64(&S.keyR[i], best);
+        }
+      }
+      return fire;
+    };
+    // Blocks of KD row-steps run branch-free (loads and DFMAs of later steps
+    // schedule across earlier ones); a block in which any lane passed the
+    // filter (about 1% with the coarse warm start) is replayed from its saved
+    // start with the per-step exact path. Every cell's arithmetic is identical.
+    for (int u = 0; u < kSH; u += KD) {
+      b1 = b0 + 1 == NB ? 0 : b0 + 1;
+      double qts[KD];
+#pragma unroll
+      for (int d = 0; d < KD; ++d) qts[d] = qt[d];
+      if constexpr (!BLK) {  // per-step vote and exact path
+#pragma unroll
+        for (int s = 0; s < KD; ++s) step(s, u, true);
+        b0 = b1;
+        continue;
+      }
+      bool any = false;
+#pragma unroll
+      for (int s = 0; s < KD; ++s) any |= step(s, u, false);
+      if (__any_sync(0xffffffffu, any)) {
+        if (P.stats && lane == 0) atomicAdd(&P.stats[0], 1ull << 40);  // replayed blocks (high bits)
+#pragma unroll
+        for (int d = 0; d < KD; ++d) qt[d] = qts[d];
+#pragma unroll
+        for (int q = 0; q < KD - 1; ++q) {  // the block-start window: columns rho0 + lane KD + q
+          const int a = q * NB + b0;
+#pragma unroll
+          for (int r = 0; r < DIMS; ++r) cv[q][r] = ring[r * R + a];
+          const double2 e = ring[DIMS * R + a];
+          ce[q] = e.x;
+          cth[q] = __double2hiint(e.y);
+        }
+#pragma unroll
+        for (int s = 0; s < KD; ++s) step(s, u, true);
+      }
+      b0 = b1;
+    }
+    if (P.stats && lane == 0) atomicAdd(&P.stats[0], (unsigned long long)kSH);  // row-steps (low bits)
+    if (t + 1 < nT) cpa_wait();
+    __syncwarp();
+  }
+}
+
+// {xc[j-1], xc[j+m-1]} per dim (j = 0: {0, xc[m-1]}), zero past the last window
+__global__ void k_build_v(const double* __restrict__ xc, long long ns, long long L, long long Lp,
+                          int dims, int m, double2* __restrict__ V) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Lp * dims) return;
+  const long long q = t / Lp, j = t % Lp;
+  const double* x = xc + q * ns;
+  V[t] = j < L ? make_double2(j > 0 ? x[j - 1] : 0.0, x[j + m - 1]) : make_double2(0.0, 0.0);
 }
 
 // Any dimension count, dims outermost: a tile of T row-steps x KD diagonals
@@ -921,6 +1168,17 @@ void launch_simple_dt(const SimpleParams& P, cudaStream_t st) {
   k_simple_dt<KD, T><<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
 }
 
+template <int KD, int DIMS, bool BLK>
+void launch_simple_ring(const SimpleParams& P, cudaStream_t st) {
+  const size_t smem = SRing<KD, DIMS>::kSmem;
+  static bool attr = false;  // once per process (calls are serialised)
+  if (!attr) {
+    cudaFuncSetAttribute(k_simple_r<KD, DIMS, BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_simple_r<KD, DIMS, BLK><<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, smem, st>>>(P);
+}
+
 void launch_simple_generic(const SimpleParams& P, cudaStream_t st) {
   k_simple<<<(unsigned)((P.n_items + kMWarps - 1) / kMWarps), kMWarps * 32, 0, st>>>(P);
 }
@@ -931,6 +1189,35 @@ bool simple_tiled(long long dims) {
   const char* t = getenv("MPGPU_SIMPLE_TILED");  // experiments: 1 forces k_simple_dt, 0 forbids it
   if (t) return atoi(t) != 0;
   return dims > 3;  // measured crossover: the register window wins for d <= 3
+}
+
+// the shared-memory ring kernel (k_simple_r) for dims <= 3; MPGPU_SIMPLE_RING=0
+// falls back to the register-window kernels (experiments)
+bool simple_ring(long long dims) {
+  const char* t = getenv("MPGPU_SIMPLE_RING");
+  if (t && atoi(t) == 0) return false;
+  return dims <= 3 && !simple_tiled(dims);
+}
+int simple_ring_kd(int dims) {
+  const char* e = getenv("MPGPU_SIMPLE_KD");
+  const int kd = e ? atoi(e) : 0;
+  if (dims == 1) return (kd == 4 || kd == 8) ? kd : 4;  // measured: KD 4 beats 8 (spills)
+  if (dims == 2) return (kd == 2 || kd == 4) ? kd : 4;
+  return 2;
+}
+template <bool BLK>
+SLaunch simple_ring_pick(int dims, int kd) {
+  if (dims == 1) return kd == 8 ? launch_simple_ring<8, 1, BLK> : launch_simple_ring<4, 1, BLK>;
+  if (dims == 2) return kd == 4 ? launch_simple_ring<4, 2, BLK> : launch_simple_ring<2, 2, BLK>;
+  return launch_simple_ring<2, 3, BLK>;
+}
+SLaunch simple_ring_launcher(int dims) {
+  // branch-free blocks + replay for d = 1 (measured 4% faster), per-step votes
+  // otherwise; MPGPU_SIMPLE_BLK=0/1 overrides (experiments)
+  const char* e = getenv("MPGPU_SIMPLE_BLK");
+  const bool blk = e ? atoi(e) == 1 : dims == 1;
+  return blk ? simple_ring_pick<true>(dims, simple_ring_kd(dims))
+             : simple_ring_pick<false>(dims, simple_ring_kd(dims));
 }
 
 SLaunch simple_launcher(int dims) {
@@ -976,6 +1263,256 @@ int simple_kd(int dims) {
 
 }  // namespace
 
+namespace {
+
+// ---- SiMPle coarse warm start -----------------------------------------------------
+// PAA of the centred data (f samples per coarse sample), zero padded to stride nsc.
+__global__ void k_paa_dims(const double* __restrict__ xc, long long ns, long long nc, long long nsc,
+                           int dims, int f, double* __restrict__ out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nsc * dims) return;
+  const long long q = t / nsc, I = t % nsc;
+  double s = 0.0;
+  if (I < nc) {
+    const double* x = xc + q * ns + I * f;
+    for (int u = 0; u < f; ++u) s += x[u];
+    s /= f;
+  }
+  out[t] = s;
+}
+
+// One warp per (coarse window I of X, coarse partner): the coarse join's
+// partner J of I gives the fine diagonals k = f (J - I) + delta, |delta| <= f/2,
+// over the f fine rows i = f I ... f I + f - 1, one lane per diagonal: a direct
+// raw dot product seeds row f I, the join's recurrence walks the rest. Values
+// use the join's own formula; the cells are ordinary cells of the join,
+// min-merged into the row keys (warp minimum) and column keys (only when they
+// improve), so they only tighten the filter: the answer is unchanged up to the
+// search's rounding, which finalize removes.
+struct Exploit {
+  const double* xcX; const double* xcY; long long nsX, nsY;
+  const double* nrmX; const double* nrmY;
+  long long LX, LY;
+  const long long* ck[2];  // coarse keys of X's coarse windows (partners in Y's coarse series)
+  long long Lc, imask_c;
+  long long* keyX;          // fine keys of X windows (partners in Y)
+  long long* keyY;          // fine keys of Y windows (partners in X)
+  long long zone;           // self-join: cells with |i - j| <= zone are skipped
+  bool self;                // self: keyX = right keys (k0), keyY = left keys (k1)
+  int n_ck, f, m, dims;
+  long long imask;
+};
+
+__global__ void k_simple_exploit(const Exploit E) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long I = w / E.n_ck;
+  const int which = (int)(w % E.n_ck);
+  if (I >= E.Lc) return;
+  const long long ck = E.ck[which][I];
+  if (ck == kNoKeyS) return;
+  const long long J = ck & E.imask_c;
+  const int f = E.f;
+  const long long i0 = (long long)f * I;
+  const long long j0 = (long long)f * J + lane - f / 2;  // this lane's column at row i0
+  const bool act = lane <= f;
+  // seed: row i0 against column j0 (windows past the end read zero padding)
+  double qt = 0.0;
+  if (act && j0 >= 0) {
+    for (int q = 0; q < E.dims; ++q) {
+      const double* a = E.xcX + q * E.nsX + i0;
+      const double* c = E.xcY + q * E.nsY + j0;
+      for (int t = 0; t < E.m; ++t) qt = fma(a[t], c[t], qt);
+    }
+  }
+  // the last coarse window also covers the fine rows past f Lc
+  const int rows = (int)(I == E.Lc - 1 ? E.LX - i0 : f);
+  for (int r = 0; r < rows; ++r) {
+    const long long i = i0 + r, j = j0 + r;
+    if (i >= E.LX) break;
+    if (r > 0 && act && j - 1 >= 0) {
+      for (int q = 0; q < E.dims; ++q) {
+        const double* a = E.xcX + q * E.nsX;
+        const double* c = E.xcY + q * E.nsY;
+        qt = fma(-a[i - 1], c[j - 1], qt);
+        qt = fma(a[i + E.m - 1], c[j + E.m - 1], qt);
+      }
+    } else if (r > 0 && act && j - 1 < 0 && j >= 0) {  // first valid column: seed directly
+      qt = 0.0;
+      for (int q = 0; q < E.dims; ++q) {
+        const double* a = E.xcX + q * E.nsX + i;
+        const double* c = E.xcY + q * E.nsY + j;
+        for (int t = 0; t < E.m; ++t) qt = fma(a[t], c[t], qt);
+      }
+    }
+    bool ok = act && j >= 0 && j < E.LY;
+    if (E.self) ok = ok && (j - i > E.zone || i - j > E.zone);
+    long long kx = kNoKeyS;
+    if (ok) {
+      const double vv = fmax(fma(-2.0, qt, E.nrmX[i] + E.nrmY[j]), 0.0);
+      if (!E.self || j > i) {
+        kx = pack_key(vv, j, E.imask);                // row i of X, partner j
+        const long long ky = pack_key(vv, i, E.imask);
+        if (ky < __ldcg(&E.keyY[j])) red_min64(&E.keyY[j], ky);
+      } else {                                        // self, j < i: pair (j, i)
+        const long long kr = pack_key(vv, i, E.imask);  // right key of j
+        if (kr < __ldcg(&E.keyX[j])) red_min64(&E.keyX[j], kr);
+        const long long kl = pack_key(vv, j, E.imask);  // left key of i
+        if (kl < __ldcg(&E.keyY[i])) red_min64(&E.keyY[i], kl);
+      }
+    }
+    kx = warp_min64(kx);
+    if (lane == 0 && kx != kNoKeyS && kx < __ldcg(&E.keyX[i])) red_min64(&E.keyX[i], kx);
+  }
+}
+
+// One SiMPle join level on device-resident centred data: energies, ring
+// vectors, keys, work items and the join launches.
+struct SimpleLevel {
+  bool self = true;
+  long long dims = 1, m = 4, zone = 0;
+  long long na = 0, nb = 0, La = 0, Lb = 0, nsa = 0, nsb = 0, Lpa = 0, Lpb = 0;
+  double *xca = nullptr, *xcb = nullptr, *nra = nullptr, *nrb = nullptr;
+  double2 *va = nullptr, *vb = nullptr;
+  long long *k0 = nullptr, *k1 = nullptr;
+  long long imask = 0;
+  bool ringk = false;
+  SimpleParams P{};
+  long long n_probe = 0;
+};
+
+// Allocations (a fixed order per call: the arena reuses blocks by position)
+// and the work items. The caller fills xca / xcb before level_prepare.
+mpgpu_status level_alloc(Arena& mem, SimpleLevel& V, cudaStream_t st) {
+  const long long pad = kSimplePad, dims = V.dims, m = V.m;
+  V.La = V.na - m + 1;
+  V.Lb = V.nb - m + 1;
+  V.nsa = V.na + pad + m;
+  V.nsb = V.nb + pad + m;
+  V.Lpa = V.La + pad;
+  V.Lpb = V.Lb + pad;
+  MM_CUDA(mem.alloc(&V.xca, dims * V.nsa));
+  MM_CUDA(mem.alloc(&V.nra, V.Lpa));
+  if (!V.self) {
+    MM_CUDA(mem.alloc(&V.xcb, dims * V.nsb));
+    MM_CUDA(mem.alloc(&V.nrb, V.Lpb));
+  }
+  const long long Lpk1 = V.self ? V.Lpa : V.Lpb;
+  MM_CUDA(mem.alloc(&V.k0, V.Lpa));
+  MM_CUDA(mem.alloc(&V.k1, Lpk1));
+  const int index_bits = std::max(1, ceil_log2ll(std::max(V.La, V.Lb)));
+  V.imask = (1LL << index_bits) - 1;
+
+  const bool tiled = simple_tiled(dims);  // k_simple_dt (dims outermost)
+  V.ringk = simple_ring(dims);           // k_simple_r (shared-memory ring)
+  const int KD = V.ringk ? simple_ring_kd((int)dims) : (tiled ? simple_dt_kd() : simple_kd((int)dims));
+  const int TR = V.ringk ? kSH : (tiled ? simple_dt_t() : KD);  // rows per item: a multiple of this
+  const bool generic = tiled && KD == 1 && TR == 1;
+  const int band = 32 * KD;
+  std::vector<MItem> items;
+  const long long seg = std::max<long long>(1024, 8 * m);
+  auto build = [&](int pass, long long klo, long long khi, long long LR, long long LC) {
+    for (long long kb = klo; kb < khi; kb += band) {
+      const long long rows = std::min(LR, LC - kb);
+      for (long long r0 = 0; r0 < rows; r0 += seg) {
+        long long nr = std::min(seg, rows - r0);
+        if (!generic) nr = (nr + TR - 1) / TR * TR;  // whole step groups (padding covers the tail)
+        items.push_back(MItem{kb, r0, (int)nr, pass});
+      }
+    }
+  };
+  SimpleParams& P = V.P;
+  P = SimpleParams{};
+  P.dims = (int)dims;
+  P.m = (int)m;
+  P.imask = V.imask;
+  if (V.ringk) {
+    MM_CUDA(mem.alloc(&V.va, dims * V.Lpa));
+    if (!V.self) MM_CUDA(mem.alloc(&V.vb, dims * V.Lpb));
+  }
+  RawSeries RA{V.xca, V.nra, V.na, V.nsa, V.La, V.va, V.Lpa};
+  RawSeries RB{V.xcb, V.nrb, V.nb, V.nsb, V.Lb, V.vb, V.Lpb};
+  if (V.self) {
+    if (V.zone + 1 < V.La) build(0, V.zone + 1, V.La, V.La, V.La);
+    P.pass[0] = SimplePass{RA, RA, V.zone + 1, V.La, V.k0, V.k1};
+  } else {
+    // pass 0: rows = B windows, columns = A windows (k >= 0); pass 1: rows = A, columns = B (k >= 1)
+    build(0, 0, V.La, V.Lb, V.La);
+    if (V.Lb > 1) build(1, 1, V.Lb, V.La, V.Lb);
+    P.pass[0] = SimplePass{RB, RA, 0, V.La, V.k1, V.k0};
+    P.pass[1] = SimplePass{RA, RB, 1, V.Lb, V.k0, V.k1};
+  }
+  sort_mitems(items);
+  // Optional probe launch (MPGPU_SIMPLE_PROBE=P > 1, experiments): every P-th
+  // band first, as its own launch, then the rest.
+  V.n_probe = 0;
+  if (V.ringk) {
+    const char* e = getenv("MPGPU_SIMPLE_PROBE");
+    const long long kProbe = e ? atoll(e) : 1;
+    if (kProbe > 1) {
+      auto mid = std::stable_partition(items.begin(), items.end(), [&](const MItem& it) {
+        return ((it.kb - (it.pass == 0 ? P.pass[0].klo : P.pass[1].klo)) / band) % kProbe == 0;
+      });
+      V.n_probe = (long long)(mid - items.begin());
+    }
+  }
+  MItem* d_items = nullptr;
+  MM_CUDA(mem.alloc(&d_items, items.size()));
+  if (!items.empty())
+    MM_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(MItem) * items.size(),
+                            cudaMemcpyHostToDevice, st));
+  P.items = d_items;
+  P.n_items = (long long)items.size();
+  return MPGPU_OK;
+}
+
+// energies, ring vectors and empty keys (xca / xcb already filled)
+void level_prepare(const SimpleLevel& V, cudaStream_t st) {
+  const int bs = 256;
+  const int dims = (int)V.dims, m = (int)V.m;
+  k_raw_energy<<<(unsigned)((V.Lpa + bs - 1) / bs), bs, 0, st>>>(V.xca, V.nsa, V.La, V.Lpa, dims, m, V.nra);
+  if (!V.self)
+    k_raw_energy<<<(unsigned)((V.Lpb + bs - 1) / bs), bs, 0, st>>>(V.xcb, V.nsb, V.Lb, V.Lpb, dims, m, V.nrb);
+  if (V.ringk) {
+    k_build_v<<<(unsigned)((V.dims * V.Lpa + bs - 1) / bs), bs, 0, st>>>(V.xca, V.nsa, V.La, V.Lpa, dims, m, V.va);
+    if (!V.self)
+      k_build_v<<<(unsigned)((V.dims * V.Lpb + bs - 1) / bs), bs, 0, st>>>(V.xcb, V.nsb, V.Lb, V.Lpb, dims, m, V.vb);
+  }
+  const long long Lk1 = V.self ? V.La : V.Lb, Lpk1 = V.self ? V.Lpa : V.Lpb;
+  k_fill_val<<<(unsigned)((V.Lpa + bs - 1) / bs), bs, 0, st>>>(V.k0, V.La, V.Lpa, kNoKeyS, kPadKey);
+  k_fill_val<<<(unsigned)((Lpk1 + bs - 1) / bs), bs, 0, st>>>(V.k1, Lk1, Lpk1, kNoKeyS, kPadKey);
+}
+
+void level_run(const SimpleLevel& V, cudaStream_t st) {
+  const SimpleParams& P = V.P;
+  if (P.n_items <= 0) return;
+  const SLaunch launch = V.ringk ? simple_ring_launcher((int)V.dims) : simple_launcher((int)V.dims);
+  if (V.n_probe > 0 && V.n_probe < P.n_items) {
+    SimpleParams Q = P;
+    Q.n_items = V.n_probe;
+    launch(Q, st);
+    Q.items = P.items + V.n_probe;
+    Q.n_items = P.n_items - V.n_probe;
+    launch(Q, st);
+  } else {
+    launch(P, st);
+  }
+}
+
+// Coarse warm start (the SiMPle analogue of k_join's K2b): join the series
+// averaged in blocks of f samples (window m / f) and seed the fine keys with
+// the fine cells around every coarse match. Off for short windows / small joins.
+long long simple_coarse_factor(const SimpleLevel& F) {
+  const char* e = getenv("MPGPU_SIMPLE_COARSE");
+  if (e && atoi(e) == 0) return 0;
+  if (!F.ringk || F.m < 64) return 0;
+  const bool forced = e && atoi(e) == 1;  // tests: on whatever the size
+  if (!forced && (double)F.La * (double)(F.self ? F.La : F.Lb) < 4e8) return 0;
+  return std::min<long long>(16, F.m / 16);
+}
+
+}  // namespace
+
 extern "C" {
 
 mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
@@ -994,22 +1531,13 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
   Arena& mem = *ar;
 
   const long long na = A->n_a, nb = self ? na : A->n_b;
-  const long long La = na - m + 1, Lb = nb - m + 1;
-  if (std::max(La, Lb) >= (1LL << 31)) return set_error(MPGPU_EUNSUPPORTED, "profile longer than 2^31");
-  const long long pad = kSimplePad;
-  const long long nsa = na + pad + m, nsb = nb + pad + m;   // padded strides
-  const long long Lpa = La + pad, Lpb = Lb + pad;
-  double *xa, *xb = nullptr, *xca, *xcb = nullptr, *nra, *nrb = nullptr, *shift;
-  long long *k0, *k1;
+  if (std::max(na, nb) - m + 1 >= (1LL << 31)) return set_error(MPGPU_EUNSUPPORTED, "profile longer than 2^31");
+  double *xa, *xb = nullptr, *shift;
   MM_CUDA(mem.alloc(&xa, dims * na));
-  MM_CUDA(mem.alloc(&xca, dims * nsa));
-  MM_CUDA(mem.alloc(&nra, Lpa));
   MM_CUDA(mem.alloc(&shift, dims));
   MM_CUDA(cudaMemcpyAsync(xa, A->a, sizeof(double) * dims * na, cudaMemcpyHostToDevice, st));
   if (!self) {
     MM_CUDA(mem.alloc(&xb, dims * nb));
-    MM_CUDA(mem.alloc(&xcb, dims * nsb));
-    MM_CUDA(mem.alloc(&nrb, Lpb));
     MM_CUDA(cudaMemcpyAsync(xb, A->b, sizeof(double) * dims * nb, cudaMemcpyHostToDevice, st));
   }
   // shared per-dim shift: the mean of A's dimension (host, from the caller's buffer)
@@ -1020,78 +1548,111 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
     sh[d] = sm / (double)na;
   }
   MM_CUDA(cudaMemcpyAsync(shift, sh.data(), sizeof(double) * dims, cudaMemcpyHostToDevice, st));
-  // self: k0 = right keys (row candidates), k1 = left keys (column candidates)
-  // AB:   k0 = A keys, k1 = B keys
-  const long long Lk1 = self ? La : Lb, Lpk1 = self ? Lpa : Lpb;
-  MM_CUDA(mem.alloc(&k0, Lpa));
-  MM_CUDA(mem.alloc(&k1, Lpk1));
-  const int index_bits = std::max(1, ceil_log2ll(std::max(La, Lb)));
-  const long long imask = (1LL << index_bits) - 1;
 
-  // compile-time dims / diagonals per lane up to 16 dims, else the generic kernel
-  const bool tiled = simple_tiled(dims);  // k_simple_dt (dims outermost)
-  const int KD = tiled ? simple_dt_kd() : simple_kd((int)dims);
-  const int TR = tiled ? simple_dt_t() : KD;  // rows per item: a multiple of this
-  const bool generic = tiled && KD == 1 && TR == 1;
-  const int band = 32 * KD;
-  std::vector<MItem> items;
-  const long long seg = std::max<long long>(1024, 8 * m);
-  auto build = [&](int pass, long long klo, long long khi, long long LR, long long LC) {
-    for (long long kb = klo; kb < khi; kb += band) {
-      const long long rows = std::min(LR, LC - kb);
-      for (long long r0 = 0; r0 < rows; r0 += seg) {
-        long long nr = std::min(seg, rows - r0);
-        if (!generic) nr = (nr + TR - 1) / TR * TR;  // whole step groups (padding covers the tail)
-        items.push_back(MItem{kb, r0, (int)nr, pass});
-      }
-    }
-  };
-  SimpleParams P{};
-  P.dims = (int)dims;
-  P.m = (int)m;
-  P.imask = imask;
-  RawSeries RA{xca, nra, na, nsa, La}, RB{xcb, nrb, nb, nsb, Lb};
-  if (self) {
-    if (A->zone + 1 < La) build(0, A->zone + 1, La, La, La);
-    P.pass[0] = SimplePass{RA, RA, A->zone + 1, La, k0, k1};
-  } else {
-    // pass 0: rows = B windows, columns = A windows (k >= 0); pass 1: rows = A, columns = B (k >= 1)
-    build(0, 0, La, Lb, La);
-    if (Lb > 1) build(1, 1, Lb, La, Lb);
-    P.pass[0] = SimplePass{RB, RA, 0, La, k1, k0};
-    P.pass[1] = SimplePass{RA, RB, 1, Lb, k0, k1};
+  // the fine level; self: k0 = right keys (row candidates), k1 = left keys
+  // (column candidates); AB: k0 = A keys, k1 = B keys
+  SimpleLevel F;
+  F.self = self;
+  F.dims = dims;
+  F.m = m;
+  F.zone = self ? A->zone : 0;
+  F.na = na;
+  F.nb = nb;
+  if (mpgpu_status e = level_alloc(mem, F, st); e != MPGPU_OK) return e;
+  const long long La = F.La, Lb = F.Lb;
+  // the coarse level (warm start), when enabled
+  const long long f = simple_coarse_factor(F);
+  SimpleLevel Cz;
+  if (f > 0) {
+    Cz.self = self;
+    Cz.dims = dims;
+    Cz.m = m / f;
+    Cz.zone = self ? (F.zone + f - 1) / f : 0;
+    Cz.na = na / f;
+    Cz.nb = nb / f;
+    if (mpgpu_status e = level_alloc(mem, Cz, st); e != MPGPU_OK) return e;
   }
-  sort_mitems(items);
-  MItem* d_items = nullptr;
-  MM_CUDA(mem.alloc(&d_items, items.size()));
-  if (!items.empty())
-    MM_CUDA(cudaMemcpyAsync(d_items, items.data(), sizeof(MItem) * items.size(),
-                            cudaMemcpyHostToDevice, st));
-  P.items = d_items;
-  P.n_items = (long long)items.size();
 
   MM_CUDA(cudaEventRecord(ar->ea, st));
   const int bs = 256;
-  k_center<<<(unsigned)((dims * nsa + bs - 1) / bs), bs, 0, st>>>(xa, na, nsa, (int)dims, shift, xca);
-  k_raw_energy<<<(unsigned)((Lpa + bs - 1) / bs), bs, 0, st>>>(xca, nsa, La, Lpa, (int)dims, (int)m, nra);
-  if (!self) {
-    k_center<<<(unsigned)((dims * nsb + bs - 1) / bs), bs, 0, st>>>(xb, nb, nsb, (int)dims, shift, xcb);
-    k_raw_energy<<<(unsigned)((Lpb + bs - 1) / bs), bs, 0, st>>>(xcb, nsb, Lb, Lpb, (int)dims, (int)m, nrb);
-  }
-  k_fill_val<<<(unsigned)((Lpa + bs - 1) / bs), bs, 0, st>>>(k0, La, Lpa, kNoKeyS, kPadKey);
-  k_fill_val<<<(unsigned)((Lpk1 + bs - 1) / bs), bs, 0, st>>>(k1, Lk1, Lpk1, kNoKeyS, kPadKey);
+  k_center<<<(unsigned)((dims * F.nsa + bs - 1) / bs), bs, 0, st>>>(xa, na, F.nsa, (int)dims, shift, F.xca);
+  if (!self)
+    k_center<<<(unsigned)((dims * F.nsb + bs - 1) / bs), bs, 0, st>>>(xb, nb, F.nsb, (int)dims, shift, F.xcb);
+  level_prepare(F, st);
   unsigned long long* d_stats = nullptr;
   if (getenv("MPGPU_STATS")) {
     MM_CUDA(mem.alloc(&d_stats, 4));
     MM_CUDA(cudaMemsetAsync(d_stats, 0, 32, st));
-    P.stats = d_stats;
   }
-  if (P.n_items > 0) simple_launcher((int)dims)(P, st);
+  if (f > 0) {
+    k_paa_dims<<<(unsigned)((dims * Cz.nsa + bs - 1) / bs), bs, 0, st>>>(F.xca, F.nsa, Cz.na, Cz.nsa,
+                                                                        (int)dims, (int)f, Cz.xca);
+    if (!self)
+      k_paa_dims<<<(unsigned)((dims * Cz.nsb + bs - 1) / bs), bs, 0, st>>>(F.xcb, F.nsb, Cz.nb, Cz.nsb,
+                                                                          (int)dims, (int)f, Cz.xcb);
+    level_prepare(Cz, st);
+    level_run(Cz, st);
+    // exploit: fine rows of A against the coarse partners (self: right and
+    // left coarse keys; AB: A's coarse keys), and B's rows for an AB-join
+    Exploit E{};
+    E.f = (int)f;
+    E.m = (int)m;
+    E.dims = (int)dims;
+    E.imask = F.imask;
+    E.imask_c = Cz.imask;
+    E.zone = F.zone;
+    E.self = self;
+    E.xcX = F.xca;
+    E.nsX = F.nsa;
+    E.nrmX = F.nra;
+    E.LX = La;
+    E.Lc = Cz.La;
+    if (self) {
+      E.xcY = F.xca;
+      E.nsY = F.nsa;
+      E.nrmY = F.nra;
+      E.LY = La;
+      E.ck[0] = Cz.k0;
+      E.ck[1] = Cz.k1;
+      E.n_ck = 2;
+      E.keyX = F.k0;
+      E.keyY = F.k1;
+    } else {
+      E.xcY = F.xcb;
+      E.nsY = F.nsb;
+      E.nrmY = F.nrb;
+      E.LY = Lb;
+      E.ck[0] = Cz.k0;
+      E.n_ck = 1;
+      E.keyX = F.k0;
+      E.keyY = F.k1;
+    }
+    if (Cz.La > 0) {
+      const long long warps = Cz.La * E.n_ck;
+      k_simple_exploit<<<(unsigned)((warps * 32 + bs - 1) / bs), bs, 0, st>>>(E);
+    }
+    if (!self && Cz.Lb > 0) {
+      Exploit G = E;
+      G.xcX = F.xcb; G.nsX = F.nsb; G.nrmX = F.nrb; G.LX = Lb; G.Lc = Cz.Lb;
+      G.xcY = F.xca; G.nsY = F.nsa; G.nrmY = F.nra; G.LY = La;
+      G.ck[0] = Cz.k1;
+      G.keyX = F.k1;
+      G.keyY = F.k0;
+      k_simple_exploit<<<(unsigned)((Cz.Lb * 32 + bs - 1) / bs), bs, 0, st>>>(G);
+    }
+  }
+  F.P.stats = d_stats;
+  level_run(F, st);
+  if (getenv("MPGPU_EXPERIMENT_TWICE") && F.P.n_items > 0) {  // experiments: a pass against final keys
+    if (d_stats) MM_CUDA(cudaMemsetAsync(d_stats, 0, 32, st));
+    level_run(F, st);
+  }
   if (d_stats) {
     unsigned long long h[4];
     MM_CUDA(cudaMemcpyAsync(h, d_stats, 32, cudaMemcpyDeviceToHost, st));
     MM_CUDA(cudaStreamSynchronize(st));
-    fprintf(stderr, "simple stats: steps %llu slow steps %llu colRED %llu rowRED %llu\n", h[0], h[1], h[2], h[3]);
+    fprintf(stderr, "simple stats: steps %llu slow steps %llu colRED %llu rowRED %llu replayed blocks %llu (coarse f=%lld)\n",
+            h[0] & ((1ull << 40) - 1), h[1], h[2], h[3], h[0] >> 40, f);
   }
   const unsigned fa = (unsigned)((La * 32 + bs - 1) / bs);
   MM_CUDA(cudaGetLastError());
@@ -1103,15 +1664,15 @@ mpgpu_status mpgpu_simple_join(const mpgpu_simple_args* A) {
   if (self) {
     MM_CUDA(mem.alloc(&ol, La));
     MM_CUDA(mem.alloc(&orr, La));
-    k_simple_finalize<<<fa, bs, 0, st>>>(xa, na, La, xa, na, k0, k1, (int)dims, (int)m, imask,
+    k_simple_finalize<<<fa, bs, 0, st>>>(xa, na, La, xa, na, F.k0, F.k1, (int)dims, (int)m, F.imask,
                                          omp_a, opi_a, ol, orr);
   } else {
     MM_CUDA(mem.alloc(&omp_b, Lb));
     MM_CUDA(mem.alloc(&opi_b, Lb));
-    k_simple_finalize<<<fa, bs, 0, st>>>(xa, na, La, xb, nb, k0, nullptr, (int)dims, (int)m,
-                                         imask, omp_a, opi_a, nullptr, nullptr);
+    k_simple_finalize<<<fa, bs, 0, st>>>(xa, na, La, xb, nb, F.k0, nullptr, (int)dims, (int)m,
+                                         F.imask, omp_a, opi_a, nullptr, nullptr);
     k_simple_finalize<<<(unsigned)((Lb * 32 + bs - 1) / bs), bs, 0, st>>>(
-        xb, nb, Lb, xa, na, k1, nullptr, (int)dims, (int)m, imask, omp_b, opi_b, nullptr, nullptr);
+        xb, nb, Lb, xa, na, F.k1, nullptr, (int)dims, (int)m, F.imask, omp_b, opi_b, nullptr, nullptr);
   }
   MM_CUDA(cudaGetLastError());
   MM_CUDA(cudaEventRecord(ar->eb, st));

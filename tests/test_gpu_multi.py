@@ -236,3 +236,23 @@ def test_simple_many_dims(mp, oracle_lib):
                            (pb, oracle_lib.simple_join(b, a, 24), b, a)):
         assert close(got.values, ref[0])[0]
         assert not raw_index_mismatches(got.index, ref[1], np.arange(got.values.size), x, y, 24)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_simple_coarse_warm_start(mp, oracle_lib, monkeypatch, d):
+    """The coarse warm start (PAA join + fine cells around its matches) forced on
+    at sizes the oracle finishes quickly: self-join with flat runs, and AB both
+    ways. Its cells are cells of the join, so the profile matches the oracle."""
+    monkeypatch.setenv("MPGPU_SIMPLE_COARSE", "1")
+    g = np.random.default_rng(300 + d)
+    a = _walk(g, d, 6000)
+    a[:, 2000:2300] = 1.5                              # flat run in every dim
+    _check_simple_self(mp, oracle_lib, a, 64, 0.5, f"coarse d={d}")
+    _check_simple_self(mp, oracle_lib, _walk(g, d, 3000), 128, 0.25, f"coarse d={d} w=128")
+    x, y = _walk(g, d, 4000), _walk(g, d, 1500)
+    px, py = mp.simple_join(x, y, 64, want_b=True)
+    for got, ref, u, v in ((px, oracle_lib.simple_join(x, y, 64), x, y),
+                           (py, oracle_lib.simple_join(y, x, 64), y, x)):
+        ok, rel = close(got.values, ref[0])
+        assert ok, f"coarse AB d={d}: values (max rel {rel:.3e})"
+        assert not raw_index_mismatches(got.index, ref[1], np.arange(got.values.size), u, v, 64)
