@@ -1743,6 +1743,48 @@ MLaunch mstomp_launcher(int D) {
   return launch_mstomp<32>;
 }
 
+// One admissible dimension: row 0 of the multidimensional profile is the
+// univariate z-normalised self-join of that dimension (the per-dim distance,
+// flat convention, exclusion zone and smallest-index ties are the same), so it
+// runs on k_join (mpgpu_join) instead of the general kernel; rows k >= 1 repeat
+// it with dim_order -1 (an exhausted selection). MPGPU_MSTOMP_K3=0 keeps the
+// general kernel (experiments, tests).
+bool mstomp_univariate() {
+  const char* e = getenv("MPGPU_MSTOMP_K3");
+  return !(e && atoi(e) == 0);
+}
+
+mpgpu_status mstomp_one_dim(const mpgpu_mstomp_args* A, int dim) {
+  const long long dims = A->dims, n = A->n, L = n - A->window + 1;
+  std::vector<double> mp(A->mp ? 0 : L);
+  std::vector<long long> pi(A->pi ? 0 : L);
+  double* mp0 = A->mp ? A->mp : mp.data();
+  long long* pi0 = A->pi ? (long long*)A->pi : pi.data();
+  const int32_t dev = A->device;
+  mpgpu_join_args J{};
+  J.a = A->x + (size_t)dim * n;
+  J.n_a = n;
+  J.window = A->window;
+  J.zone = A->zone;
+  J.n_gpus = 1;
+  J.devices = &dev;
+  J.mp_a = mp0;
+  J.pi_a = (int64_t*)pi0;
+  double kms = 0.0;
+  if (mpgpu_status e = mpgpu_join_timed(&J, &kms, nullptr); e != MPGPU_OK) return e;
+  for (long long k = 1; k < dims; ++k) {
+    if (A->mp) std::memcpy(A->mp + k * L, mp0, sizeof(double) * L);
+    if (A->pi) std::memcpy(A->pi + k * L, pi0, sizeof(long long) * L);
+  }
+  if (A->dim_order) {
+    for (long long i = 0; i < L; ++i) A->dim_order[i] = pi0[i] >= 0 ? dim : -1;
+    for (long long k = 1; k < dims; ++k)
+      std::fill(A->dim_order + k * L, A->dim_order + (k + 1) * L, (int64_t)-1);
+  }
+  if (A->kernel_ms) *A->kernel_ms = kms;
+  return MPGPU_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1779,6 +1821,7 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
   if (D == 0) return set_error(MPGPU_EPARAM, "every dimension is excluded");
   if (D > kMaxMDims) return set_error(MPGPU_EUNSUPPORTED, "more than 32 admissible dimensions");
   const int n_must = (int)A->n_must;
+  if (D == 1 && mstomp_univariate()) return mstomp_one_dim(A, perm[0]);
   std::lock_guard<std::mutex> lk(g_multi_mu);
   MM_CUDA(cudaSetDevice(A->device));
   Arena* ar = nullptr;

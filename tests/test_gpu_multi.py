@@ -256,3 +256,21 @@ def test_simple_coarse_warm_start(mp, oracle_lib, monkeypatch, d):
         ok, rel = close(got.values, ref[0])
         assert ok, f"coarse AB d={d}: values (max rel {rel:.3e})"
         assert not raw_index_mismatches(got.index, ref[1], np.arange(got.values.size), u, v, 64)
+
+
+def test_mstomp_one_admissible_dim_on_k_join(mp, oracle_lib, monkeypatch):
+    """One admissible dimension runs on the univariate join (k_join): same
+    profile as the general mSTOMP kernel and the oracle, flat windows and an
+    excluded dimension included (rows k >= 1 repeat row 0, dim_order -1)."""
+    g = np.random.default_rng(91)
+    x = _walk(g, 1, 3000)
+    x[0, 1000:1200] = 2.0
+    got = _check_mstomp(mp, oracle_lib, x, 64, label="d=1 on k_join")
+    y = _walk(g, 3, 2000)
+    y[1, 500:700] = -1.0
+    got3 = _check_mstomp(mp, oracle_lib, y, 32, exc=(0, 2), label="exc -> D=1 on k_join")
+    assert np.all(got3.dim_order[1:] == -1) and np.array_equal(got3.values[1], got3.values[0])
+    monkeypatch.setenv("MPGPU_MSTOMP_K3", "0")
+    ref = mp.mstomp(x, 64, 0.5)
+    assert np.allclose(ref.values, got.values, rtol=1e-9, atol=1e-9)
+    assert np.array_equal(ref.dim_order, got.dim_order)
