@@ -193,8 +193,9 @@ if __name__ == "__main__":
     if not only or "fluss" in only:
         fluss_row()
     if not only or "multi" in only:
-        for d in (1, 3):
-            multivariate_row("mstomp", d, 1 << 16, 256, 12 * d,
-                             f"per dim 2 recurrence + 2 normalise + 1 distance + 5 sqrt + 2 prefix mean")
+        # one admissible dim runs on k_join: SURVEY §8(d)'s 6 fp64-pipe ops per cell
+        multivariate_row("mstomp", 1, 1 << 16, 256, 6, "k_join (one admissible dim): SURVEY 8(d) count")
+        multivariate_row("mstomp", 3, 1 << 16, 256, 36,
+                         "per dim 2 recurrence + 2 normalise + 1 distance + 5 sqrt + 2 prefix mean")
         for d, n, m in ((1, 1 << 17, 256), (3, 1 << 16, 256), (12, 1 << 15, 64)):
             multivariate_row("simple", d, n, m, 2 * d + 2, "2 per dim recurrence + add + distance")
