@@ -285,19 +285,18 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_t(const SimpleParams
 // DIMS planes of V = {x[j-1], x[j+m-1]} plus {energy, key}, each plane
 // blocked-transposed so the 32 lanes' entering columns are 32 consecutive
 // 16-byte slots (conflict-free LDS.128). Rows are broadcast loads.
-constexpr int kSH = 32;  // rows per tile
-
 template <int KD, int DIMS>
 struct SRing {
+  static constexpr int TS = DIMS <= 3 ? 32 : 16;                        // rows per tile
   static constexpr int kWs = 32 * KD;                                   // diagonals per band
-  static constexpr int R = ((kWs + 2 * kSH + KD - 1) / KD) * KD;        // ring slots
+  static constexpr int R = ((kWs + 2 * TS + KD - 1) / KD) * KD;         // ring slots
   static constexpr int NB = R / KD;
   static constexpr int kPlanes = DIMS + 1;
-  static constexpr int kRowPlane = kSH + 1;
+  static constexpr int kRowPlane = TS + 1;
   static constexpr int kPerWarp = kPlanes * R + 2 * kPlanes * kRowPlane;  // double2 per warp
   static constexpr size_t kSmem = sizeof(double2) * kPerWarp * kMWarps;
   // rows padded to whole tiles and the band's last columns stay inside the padding
-  static_assert(kWs + kSH <= kSimplePad, "padding too short for the ring kernel");
+  static_assert(kWs + TS <= kSimplePad, "padding too short for the ring kernel");
 };
 
 __device__ __forceinline__ unsigned sm_u32(const void* p) {
@@ -314,7 +313,7 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_all;\n"
 template <int KD, int DIMS, bool BLK>
 __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_r(const SimpleParams P) {
   using G = SRing<KD, DIMS>;
-  constexpr int R = G::R, NB = G::NB, NP = G::kPlanes, RP = G::kRowPlane, kWs = G::kWs;
+  constexpr int R = G::R, NB = G::NB, NP = G::kPlanes, RP = G::kRowPlane, kWs = G::kWs, kSH = G::TS;
   extern __shared__ double2 sring[];
   double2* const ring = sring + (threadIdx.x >> 5) * G::kPerWarp;  // plane e at ring + e R
   double2* const rows = ring + NP * R;                              // (buf NP + e) RP + h
@@ -351,7 +350,7 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_r(const SimpleParams
   };
 
   // tile 0 in flight while the seeds are computed
-  fetch_row(0, lane, r0 + lane);
+  if (lane < kSH) fetch_row(0, lane, r0 + lane);
   for (int x = lane; x < kSH + kWs - 1; x += 32) fetch_col(x);
 
   // seeds: QT(r0, c0 + d) by direct dot products over all dims
@@ -393,8 +392,10 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_simple_r(const SimpleParams
     const int buf = t & 1;
     const int ts = t * kSH;
     if (t + 1 < nT) {
-      fetch_row(buf ^ 1, lane, r0 + ts + kSH + lane);
-      fetch_col(ts + kSH + kWs - 1 + lane);
+      if (lane < kSH) {
+        fetch_row(buf ^ 1, lane, r0 + ts + kSH + lane);
+        fetch_col(ts + kSH + kWs - 1 + lane);
+      }
     }
     int b0 = (int)((ts / KD + lane) % NB), b1 = 0;
     // One row-step: the entering column and the row from the ring, the
@@ -1191,33 +1192,56 @@ bool simple_tiled(long long dims) {
   return dims > 3;  // measured crossover: the register window wins for d <= 3
 }
 
-// the shared-memory ring kernel (k_simple_r) for dims <= 3; MPGPU_SIMPLE_RING=0
-// falls back to the register-window kernels (experiments)
+// the shared-memory ring kernel (k_simple_r) for dims <= kRingMaxDims;
+// MPGPU_SIMPLE_RING=0 falls back to the register-window / tiled kernels
+// (experiments), as does an explicit MPGPU_SIMPLE_TILED=1
+constexpr int kRingMaxDims = 12;
 bool simple_ring(long long dims) {
   const char* t = getenv("MPGPU_SIMPLE_RING");
   if (t && atoi(t) == 0) return false;
-  return dims <= 3 && !simple_tiled(dims);
+  const char* u = getenv("MPGPU_SIMPLE_TILED");
+  if (u && atoi(u) == 1) return false;
+  return dims <= kRingMaxDims;
 }
+int simple_ring_ts(int dims) { return dims <= 3 ? 32 : 16; }  // SRing<.., dims>::TS
 int simple_ring_kd(int dims) {
   const char* e = getenv("MPGPU_SIMPLE_KD");
   const int kd = e ? atoi(e) : 0;
   if (dims == 1) return (kd == 4 || kd == 8) ? kd : 4;  // measured: KD 4 beats 8 (spills)
   if (dims == 2) return (kd == 2 || kd == 4) ? kd : 4;
-  return 2;
+  return dims <= 8 ? 2 : 1;
 }
 template <bool BLK>
 SLaunch simple_ring_pick(int dims, int kd) {
-  if (dims == 1) return kd == 8 ? launch_simple_ring<8, 1, BLK> : launch_simple_ring<4, 1, BLK>;
-  if (dims == 2) return kd == 4 ? launch_simple_ring<4, 2, BLK> : launch_simple_ring<2, 2, BLK>;
-  return launch_simple_ring<2, 3, BLK>;
+  switch (dims) {
+    case 1: return kd == 8 ? launch_simple_ring<8, 1, BLK> : launch_simple_ring<4, 1, BLK>;
+    case 2: return kd == 4 ? launch_simple_ring<4, 2, BLK> : launch_simple_ring<2, 2, BLK>;
+    case 3: return launch_simple_ring<2, 3, BLK>;
+    default: break;
+  }
+  if constexpr (BLK) {
+    return nullptr;  // block replay is instantiated for dims <= 3 only
+  } else {
+    switch (dims) {
+      case 4: return launch_simple_ring<2, 4, BLK>;
+      case 5: return launch_simple_ring<2, 5, BLK>;
+      case 6: return launch_simple_ring<2, 6, BLK>;
+      case 7: return launch_simple_ring<2, 7, BLK>;
+      case 8: return launch_simple_ring<2, 8, BLK>;
+      case 9: return launch_simple_ring<1, 9, BLK>;
+      case 10: return launch_simple_ring<1, 10, BLK>;
+      case 11: return launch_simple_ring<1, 11, BLK>;
+      default: return launch_simple_ring<1, 12, BLK>;
+    }
+  }
 }
 SLaunch simple_ring_launcher(int dims) {
   // branch-free blocks + replay for d = 1 (measured 4% faster), per-step votes
   // otherwise; MPGPU_SIMPLE_BLK=0/1 overrides (experiments)
   const char* e = getenv("MPGPU_SIMPLE_BLK");
   const bool blk = e ? atoi(e) == 1 : dims == 1;
-  return blk ? simple_ring_pick<true>(dims, simple_ring_kd(dims))
-             : simple_ring_pick<false>(dims, simple_ring_kd(dims));
+  return (blk && dims <= 3) ? simple_ring_pick<true>(dims, simple_ring_kd(dims))
+                            : simple_ring_pick<false>(dims, simple_ring_kd(dims));
 }
 
 SLaunch simple_launcher(int dims) {
@@ -1406,7 +1430,7 @@ mpgpu_status level_alloc(Arena& mem, SimpleLevel& V, cudaStream_t st) {
   const bool tiled = simple_tiled(dims);  // k_simple_dt (dims outermost)
   V.ringk = simple_ring(dims);           // k_simple_r (shared-memory ring)
   const int KD = V.ringk ? simple_ring_kd((int)dims) : (tiled ? simple_dt_kd() : simple_kd((int)dims));
-  const int TR = V.ringk ? kSH : (tiled ? simple_dt_t() : KD);  // rows per item: a multiple of this
+  const int TR = V.ringk ? simple_ring_ts((int)dims) : (tiled ? simple_dt_t() : KD);  // rows per item: a multiple of this
   const bool generic = tiled && KD == 1 && TR == 1;
   const int band = 32 * KD;
   std::vector<MItem> items;

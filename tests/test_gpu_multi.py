@@ -225,8 +225,12 @@ def test_mstomp_constant_series(mp, oracle_lib):
     assert np.array_equal(r.index, ref[1])           # smallest admissible partner, as the oracle
 
 
-def test_simple_many_dims(mp, oracle_lib):
-    """d > 8 runs the dims-outermost tiled kernel (k_simple_dt)."""
+@pytest.mark.parametrize("ring", ["1", "0"])
+def test_simple_many_dims(mp, oracle_lib, monkeypatch, ring):
+    """d = 9-12 runs the ring kernel with one diagonal per lane (k_simple_r<1, d>);
+    with the ring off (and above 12 dims) the dims-outermost tiled kernel
+    (k_simple_dt) runs."""
+    monkeypatch.setenv("MPGPU_SIMPLE_RING", ring)
     g = np.random.default_rng(71)
     _check_simple_self(mp, oracle_lib, _walk(g, 10, 700), 20, 0.5, "d=10")
     _check_simple_self(mp, oracle_lib, g.uniform(0, 1, (12, 900)), 16, 0.25, "d=12 uniform")
@@ -274,3 +278,10 @@ def test_mstomp_one_admissible_dim_on_k_join(mp, oracle_lib, monkeypatch):
     ref = mp.mstomp(x, 64, 0.5)
     assert np.allclose(ref.values, got.values, rtol=1e-9, atol=1e-9)
     assert np.array_equal(ref.dim_order, got.dim_order)
+
+
+def test_simple_above_ring_dims(mp, oracle_lib):
+    """More than 12 dims: the tiled kernel by default."""
+    g = np.random.default_rng(73)
+    _check_simple_self(mp, oracle_lib, _walk(g, 14, 600), 16, 0.5, "d=14")
+
