@@ -182,7 +182,8 @@ void build_items(mpgpu_plan* p) {
   // small (8m rows -> ~6%), short enough that every warp-worker gets at least
   // two items, and at most 64 items per worker on big joins.
   const long long seg_balance = cells / ((long long)kW * 64 * ref_workers);
-  const long long seg_fill = cells / ((long long)kW * 2 * ref_workers);
+  static const long long fill_items = getenv("MPGPU_SEG_FILL") ? atoll(getenv("MPGPU_SEG_FILL")) : 2;
+  const long long seg_fill = cells / ((long long)kW * fill_items * ref_workers);
   long long seg = std::max(seg_balance, std::min<long long>(8 * p->m, seg_fill));
   seg = std::min<long long>(std::max<long long>(16384, 8 * p->m), seg);
   // at most ~1e8 items (2.4 GB of item records; the queue index is an int):
