@@ -793,6 +793,7 @@ struct MStompParams {
   int m, n_must;
   int D;              // admissible dims (<= the kernel's capacity)
   long long imask;
+  unsigned long long* stats;  // MPGPU_STATS=1: [row-steps, exact row-steps]
 };
 
 // element index of (window j, dim 0) in the blocked layout; dim q adds 32 q
@@ -813,6 +814,36 @@ __device__ __forceinline__ void sort_keys(unsigned long long (&s)[D]) {
       s[q + 1] = sw ? a : b;
     }
   }
+}
+
+// the same network on 32-bit keys, min / max per compare-exchange (the fast pass)
+template <int D>
+__device__ __forceinline__ void sort_u32(unsigned (&s)[D]) {
+#pragma unroll
+  for (int r = 0; r < D; ++r) {
+#pragma unroll
+    for (int q = (r & 1); q + 1 < D; q += 2) {
+      const unsigned a = s[q], b = s[q + 1];
+      s[q] = min(a, b);
+      s[q + 1] = max(a, b);
+    }
+  }
+}
+
+// fp32 search distance for the fast pass: s = 2m(1 - corr) >= 0 (clamped below
+// at 2^-100: its high word turned into fp32 bits by one LEA, 20 mantissa bits,
+// truncated) and the approximate fp32 square root (MUFU.SQRT)
+constexpr int kTinyHi = (1023 - 100) << 20;
+__device__ __forceinline__ float dist_fast(double s) {
+  const int h = max(__double2hiint(s), kTinyHi);
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__int_as_float((h << 3) - (896 << 23))));
+  return r;
+}
+// high word of the fp64 value nearest an fp32 value (positive normal): the
+// fast pass compares it with the keys' high words like the exact pass
+__device__ __forceinline__ int hi_of_f32(float f) {
+  return (int)((unsigned)__float_as_int(f) >> 3) + (896 << 20);
 }
 
 template <int D>
@@ -966,33 +997,58 @@ __global__ void __launch_bounds__(kMWarps * 32, 2) k_mstomp_t(const MStompParams
         ri[q] = P.WI[ei + 32 * q];
         rth[q] = __ldcg(khi_ + 2 * (ei + 32 * q));
       }
-      double pk[KD][D];
+      // covariance recurrences (exact, fp64), then the fast filter in fp32:
+      // the prefix means from fp32 distances (relative error below 2^-19.5:
+      // 2^-20 from the truncated s, 2^-22 from the square root and the fp32
+      // sums) compared with thresholds raised by kFastSlack high-word units
+      // (2^-20 each), so it never skips a cell the exact test takes; a
+      // row-step where any lane passes recomputes every value exactly.
+      constexpr int kFastSlack = 4;
       bool fire = false;
 #pragma unroll
       for (int d = 0; d < KD; ++d) {
         const int sl = (s + d) % KD;
-        unsigned long long sk[D];
+        unsigned sf[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) {
           cov[d][q] = fma(ru[q].x, cu[sl][q].y, cov[d][q]);
           cov[d][q] = fma(ru[q].y, cu[sl][q].x, cov[d][q]);
-          // corr with the flat convention (distance.hpp:14-15): inv = 0 for a flat
-          // window and the halves add 1 (both flat: d = 0) or 1/2 (one: d = sqrt(m))
           const double corr = fma(cov[d][q], ri[q].x * ci[sl][q].x, ri[q].y + ci[sl][q].y);
-          sk[q] = (unsigned long long)__double_as_longlong(sqrt_search(clamp0(fma(-two_m, corr, two_m)))) |
-                  (q >= P.n_must ? kFree : 0ULL);
+          sf[q] = (unsigned)__float_as_int(dist_fast(fma(-two_m, corr, two_m))) |
+                  (q >= P.n_must ? 0x80000000u : 0u);
         }
-        sort_keys<D>(sk);
-        double acc = 0.0;
+        sort_u32<D>(sf);
+        float acc = 0.0f;
 #pragma unroll
         for (int q = 0; q < D; ++q) {
-          acc += __longlong_as_double((long long)(sk[q] & ~kFree));
-          pk[d][q] = acc * (1.0 / (double)(q + 1));
-          const int h = __double2hiint(pk[d][q]);
+          acc += __int_as_float((int)(sf[q] & 0x7fffffffu));
+          const int h = hi_of_f32(acc * (1.0f / (float)(q + 1))) - kFastSlack;
           fire |= (h <= rth[q]) | (h <= cth[sl][q]);
         }
       }
+      if (P.stats && lane == 0) atomicAdd(&P.stats[0], 1ull);
       if (__any_sync(0xffffffffu, fire)) {
+        if (P.stats && lane == 0) atomicAdd(&P.stats[1], 1ull);
+        // exact values of the row-step (the cov recurrences above are exact)
+        double pk[KD][D];
+#pragma unroll
+        for (int d = 0; d < KD; ++d) {
+          const int sl = (s + d) % KD;
+          unsigned long long sk[D];
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            const double corr = fma(cov[d][q], ri[q].x * ci[sl][q].x, ri[q].y + ci[sl][q].y);
+            sk[q] = (unsigned long long)__double_as_longlong(sqrt_search(clamp0(fma(-two_m, corr, two_m)))) |
+                    (q >= P.n_must ? kFree : 0ULL);
+          }
+          sort_keys<D>(sk);
+          double a = 0.0;
+#pragma unroll
+          for (int q = 0; q < D; ++q) {
+            a += __longlong_as_double((long long)(sk[q] & ~kFree));
+            pk[d][q] = a * (1.0 / (double)(q + 1));
+          }
+        }
         long long best[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) best[q] = kNoKeyS;
@@ -1914,7 +1970,21 @@ mpgpu_status mpgpu_mstomp(const mpgpu_mstomp_args* A) {
   const int bs = 256;
   k_build_w<<<(unsigned)((Lb * D + bs - 1) / bs), bs, 0, st>>>(U, inv, L, Lp, Lb, D, WU, WI, keys);
   MM_CUDA(cudaGetLastError());
+  unsigned long long* d_stats = nullptr;
+  if (getenv("MPGPU_STATS")) {
+    MM_CUDA(mem.alloc(&d_stats, 2));
+    MM_CUDA(cudaMemsetAsync(d_stats, 0, 16, st));
+    P.stats = d_stats;
+  }
   if (P.n_items > 0) mstomp_launcher(D)(P, st);
+  if (d_stats) {
+    unsigned long long h[2];
+    MM_CUDA(cudaMemcpyAsync(h, d_stats, 16, cudaMemcpyDeviceToHost, st));
+    MM_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "mstomp stats: warp row-steps %llu exact row-steps %llu (%.2f%%)\n", h[0], h[1],
+            100.0 * (double)h[1] / (double)(h[0] ? h[0] : 1));
+  }
+  if (P.n_items > 0 && getenv("MPGPU_EXPERIMENT_TWICE")) mstomp_launcher(D)(P, st);  // vs final keys
   MM_CUDA(cudaGetLastError());
   const long long outs = (long long)dims * L;
   k_mstomp_finalize<<<(unsigned)((outs * 32 + bs - 1) / bs), bs, 0, st>>>(P, D, (int)dims, dperm,
