@@ -20,8 +20,14 @@ def merge_keys_(row_keys, col_keys, group=None, root: Optional[int] = None) -> N
     to `root` only."""
     import torch.distributed as dist
     op = dist.ReduceOp.MIN
+    host_staged = row_keys.is_cuda and dist.get_backend(group) == "gloo"
     for t in (row_keys, col_keys):
-        if root is None:
+        if host_staged:
+            # gloo (functional tests only: two ranks sharing one GPU) reduces host tensors
+            h = t.cpu()
+            dist.all_reduce(h, op=op, group=group)
+            t.copy_(h)
+        elif root is None:
             dist.all_reduce(t, op=op, group=group)
         else:
             dist.reduce(t, dst=root, op=op, group=group)

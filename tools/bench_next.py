@@ -197,5 +197,7 @@ if __name__ == "__main__":
         multivariate_row("mstomp", 1, 1 << 16, 256, 6, "k_join (one admissible dim): SURVEY 8(d) count")
         multivariate_row("mstomp", 3, 1 << 16, 256, 36,
                          "per dim 2 recurrence + 2 normalise + 1 distance + 5 sqrt + 2 prefix mean")
+        multivariate_row("mstomp", 8, 1 << 15, 128, 96,
+                         "per dim 2 recurrence + 2 normalise + 1 distance + 5 sqrt + 2 prefix mean")
         for d, n, m in ((1, 1 << 17, 256), (3, 1 << 16, 256), (8, 1 << 16, 128), (12, 1 << 15, 64)):
             multivariate_row("simple", d, n, m, 2 * d + 2, "2 per dim recurrence + add + distance")
