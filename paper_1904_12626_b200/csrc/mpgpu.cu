@@ -835,22 +835,50 @@ mpgpu_status argext(const double* d_v, long long n, int sign, cudaStream_t st, d
 }
 }  // namespace
 
+namespace {
+// FLUSS scratch (the 32-bit arc-end differences and the tile sums), kept per
+// device across calls: a fresh 4 B/window allocation per call costs more than
+// the whole sweep once the memory pool trims it. Calls on a device are
+// serialised and each waits on the previous call's use of the buffer.
+struct FlussScratch {
+  std::mutex mu;
+  char* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+};
+FlussScratch g_fluss[64];
+}  // namespace
+
 mpgpu_status mpgpu_fluss(const int64_t* d_index, int64_t L, int64_t window, int64_t* d_arcs,
                          double* d_cac, int32_t device, void* cuda_stream) {
   if (!d_index || !d_arcs || L < 1 || window < 0) return fail(MPGPU_EPARAM, "bad FLUSS arguments");
   MPG_CUDA(cudaSetDevice(device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  MPG_CUDA(cudaMemsetAsync(d_arcs, 0, sizeof(long long) * L, st));
-  k_arc_ends<<<(unsigned)((L + 255) / 256), 256, 0, st>>>((const long long*)d_index, L,
-                                                         (long long*)d_arcs);
+  if (L >= (1ll << 31)) return fail(MPGPU_EPARAM, "FLUSS: L must be below 2^31");
+  if (device < 0 || device >= 64) return fail(MPGPU_EPARAM, "device out of range");
   const long long nt = (L + kScanTile - 1) / kScanTile;
-  long long* sums = nullptr;
-  if (cudaMallocAsync(&sums, sizeof(long long) * nt, st) != cudaSuccess)
-    return fail(MPGPU_ENOMEM, "FLUSS scan scratch");
-  k_scan_tile_sums<<<(unsigned)nt, kScanThreads, 0, st>>>((const long long*)d_arcs, L, sums);
+  const size_t need = sizeof(long long) * nt + sizeof(int) * L;
+  FlussScratch& F = g_fluss[device];
+  std::lock_guard<std::mutex> lk(F.mu);
+  if (!F.done) MPG_CUDA(cudaEventCreateWithFlags(&F.done, cudaEventDisableTiming));
+  if (F.cap < need) {
+    MPG_CUDA(cudaEventSynchronize(F.done));
+    if (F.p) MPG_CUDA(cudaFree(F.p));
+    F.p = nullptr;
+    F.cap = 0;
+    if (cudaMalloc(&F.p, need) != cudaSuccess) return fail(MPGPU_ENOMEM, "FLUSS scratch");
+    F.cap = need;
+  }
+  MPG_CUDA(cudaStreamWaitEvent(st, F.done, 0));
+  long long* sums = reinterpret_cast<long long*>(F.p);
+  int* diff = reinterpret_cast<int*>(sums + nt);
+  MPG_CUDA(cudaMemsetAsync(diff, 0, sizeof(int) * L, st));
+  k_arc_far_ends<<<(unsigned)((L + 255) / 256), 256, 0, st>>>((const long long*)d_index, L, diff);
+  k_scan_tile_sums<<<(unsigned)nt, kScanThreads, 0, st>>>((const long long*)d_index, diff, L, sums);
   k_scan_sums<<<1, 1024, 0, st>>>(sums, nt);
-  k_scan_tile_apply<<<(unsigned)nt, kScanThreads, 0, st>>>((long long*)d_arcs, L, sums, window, d_cac);
-  cudaFreeAsync(sums, st);
+  k_scan_tile_apply<<<(unsigned)nt, kScanThreads, 0, st>>>((const long long*)d_index, diff, L, sums,
+                                                           window, (long long*)d_arcs, d_cac);
+  MPG_CUDA(cudaEventRecord(F.done, st));
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
 }

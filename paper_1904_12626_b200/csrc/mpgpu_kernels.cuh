@@ -907,28 +907,53 @@ __global__ void __launch_bounds__(kMassThreads) k_mass(
 
 // ---- K7: matrix-profile consumers (discovery.hpp:61-79) -----------------------
 // FLUSS arc count: every nearest-neighbour arc (i, index[i]) adds +1 on the open
-// interval strictly between its endpoints (a +1/-1 sweep, discovery.hpp:68-70).
-__global__ void k_arc_ends(const long long* __restrict__ index, long long L,
-                           long long* __restrict__ diff) {
+// interval strictly between its endpoints (a +1/-1 sweep, discovery.hpp:68-70):
+// +1 at lo + 1, -1 at hi, for hi - lo >= 2. One of the two ends is always next
+// to the arc's own window: +1 at i + 1 when index[i] > i, -1 at i when
+// index[i] < i. That end is computed in the scan passes from index[k - 1] and
+// index[k] (coalesced, no atomic); only the far end is a random RED.ADD into a
+// 32-bit difference array (4 B per window, L2-resident up to L ~ 2^24).
+__device__ __forceinline__ bool arc_ok(long long i, long long j, long long L) {
+  return j >= 0 && j < L && (j - i >= 2 || i - j >= 2);
+}
+
+__global__ void k_arc_far_ends(const long long* __restrict__ index, long long L,
+                               int* __restrict__ diff) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= L) return;
   const long long j = index[i];
-  if (j < 0 || j >= L || j == i) return;
-  const long long lo = i < j ? i : j, hi = i < j ? j : i;
-  if (hi - lo < 2) return;
-  atomicAdd((unsigned long long*)&diff[lo + 1], 1ull);
-  atomicAdd((unsigned long long*)&diff[hi], (unsigned long long)-1LL);
+  if (!arc_ok(i, j, L)) return;
+  if (j > i) {
+    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(diff + j), "r"(-1));
+  } else {
+    asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(diff + j + 1), "r"(1));
+  }
+}
+
+// diff[k] plus the near ends at k: +1 from the arc of window k - 1 pointing
+// right, -1 from the arc of window k pointing left.
+__device__ __forceinline__ long long arc_delta(const long long* __restrict__ index,
+                                               const int* __restrict__ diff, long long k, long long L) {
+  long long v = diff[k];
+  const long long jk = index[k];
+  if (arc_ok(k, jk, L) && jk < k) v -= 1;
+  if (k > 0) {
+    const long long jp = index[k - 1];
+    if (arc_ok(k - 1, jp, L) && jp > k - 1) v += 1;
+  }
+  return v;
 }
 
 // Inclusive prefix sum of the arc-end differences, in three coalesced passes:
 // per-tile sums, a scan of the tile sums, then each tile rescanned with its
 // offset. The last pass also writes the corrected arc curve (CAC), so the arc
-// counts are read once. 32 B of traffic per window plus the arc-end atomics.
+// counts are written once.
 constexpr int kScanThreads = 256;
 constexpr int kScanPer = 16;
 constexpr int kScanTile = kScanThreads * kScanPer;  // 4096 windows per block
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(const long long* __restrict__ a,
+__global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(const long long* __restrict__ index,
+                                                                 const int* __restrict__ diff,
                                                                  long long L,
                                                                  long long* __restrict__ sums) {
   __shared__ long long ws[kScanThreads / 32];
@@ -937,7 +962,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(const long long
 #pragma unroll
   for (int q = 0; q < kScanPer; ++q) {
     const long long i = base + q * kScanThreads + threadIdx.x;
-    if (i < L) s += a[i];
+    if (i < L) s += arc_delta(index, diff, i, L);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -950,26 +975,35 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tile_sums(const long long
   }
 }
 
-// Exclusive scan of the n tile sums in one block (n = L / 4096: 2048 at 2^23).
-__global__ void k_scan_sums(long long* __restrict__ sums, long long n) {
-  __shared__ long long tot[1024];
+// Exclusive scan of the n tile sums in one block of 1024 threads (n = L / 4096:
+// 2048 at 2^23): each thread sums a contiguous chunk, the chunk totals are
+// scanned with warp shuffles, then each chunk is rewritten with its offset.
+__global__ void __launch_bounds__(1024) k_scan_sums(long long* __restrict__ sums, long long n) {
+  __shared__ long long wtot[32];
   const int t = threadIdx.x, nt = blockDim.x;
   const long long chunk = (n + nt - 1) / nt;
   const long long lo = t * chunk, hi = lo + chunk < n ? lo + chunk : n;
   long long s = 0;
   for (long long i = lo; i < hi; ++i) s += sums[i];
-  tot[t] = s;
+  long long x = s;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((t & 31) >= o) x += y;
+  }
+  if ((t & 31) == 31) wtot[t >> 5] = x;
   __syncthreads();
-  if (t == 0) {
-    long long run = 0;
-    for (int q = 0; q < nt; ++q) {
-      const long long v = tot[q];
-      tot[q] = run;
-      run += v;
+  if (t < 32) {
+    long long w = wtot[t], v = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, v, o);
+      if (t >= o) v += y;
     }
+    wtot[t] = v - w;  // exclusive over warps
   }
   __syncthreads();
-  long long run = tot[t];
+  long long run = wtot[t >> 5] + (x - s);
   for (long long i = lo; i < hi; ++i) {
     const long long v = sums[i];
     sums[i] = run;
@@ -989,26 +1023,33 @@ __device__ __forceinline__ double cac_of(long long arcs, long long i, long long 
   return v;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_tile_apply(long long* __restrict__ a, long long L,
+__global__ void __launch_bounds__(kScanThreads) k_scan_tile_apply(const long long* __restrict__ index,
+                                                                  const int* __restrict__ diff,
+                                                                  long long L,
                                                                   const long long* __restrict__ offs,
                                                                   long long window,
+                                                                  long long* __restrict__ a,
                                                                   double* __restrict__ cac) {
-  __shared__ long long tile[kScanTile];
+  // rows of kScanPer entries padded to kScanPer + 1: the coalesced phase writes
+  // consecutive words, and the per-thread row reads of a half-warp hit 16
+  // distinct 8-byte banks
+  static_assert(kScanPer == 16, "padding written for 16 entries per thread");
+  __shared__ long long tile[kScanTile / kScanPer * (kScanPer + 1)];
   __shared__ long long ws[kScanThreads / 32];
+  auto P = [](int k) { return (k >> 4) * (kScanPer + 1) + (k & 15); };
   const long long base = (long long)blockIdx.x * kScanTile;
 #pragma unroll
   for (int q = 0; q < kScanPer; ++q) {  // coalesced load
     const int k = q * kScanThreads + threadIdx.x;
-    tile[k] = base + k < L ? a[base + k] : 0;
+    tile[P(k)] = base + k < L ? arc_delta(index, diff, base + k, L) : 0;
   }
   __syncthreads();
-  // each thread scans kScanPer consecutive entries (a small bank conflict per
-  // step; the pass is bandwidth-bound)
+  // each thread scans kScanPer consecutive entries
   long long v[kScanPer];
   long long s = 0;
 #pragma unroll
   for (int q = 0; q < kScanPer; ++q) {
-    s += tile[threadIdx.x * kScanPer + q];
+    s += tile[threadIdx.x * (kScanPer + 1) + q];
     v[q] = s;
   }
   // exclusive scan of the thread totals across the block
@@ -1024,16 +1065,16 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_tile_apply(long long* __r
   for (int w = 0; w < (threadIdx.x >> 5); ++w) wpre += ws[w];
   const long long pre = offs[blockIdx.x] + wpre + (x - s);
 #pragma unroll
-  for (int q = 0; q < kScanPer; ++q) tile[threadIdx.x * kScanPer + q] = v[q] + pre;
+  for (int q = 0; q < kScanPer; ++q) tile[threadIdx.x * (kScanPer + 1) + q] = v[q] + pre;
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < kScanPer; ++q) {  // coalesced store (+ the CAC)
     const int k = q * kScanThreads + threadIdx.x;
     const long long i = base + k;
     if (i < L) {
-      const long long arcs = tile[k];
-      a[i] = arcs;
-      if (cac) cac[i] = cac_of(arcs, i, L, window);
+      const long long arcs = tile[P(k)];
+      __stcs(a + i, arcs);
+      if (cac) __stcs(cac + i, cac_of(arcs, i, L, window));
     }
   }
 }

@@ -59,3 +59,21 @@ def test_fluss_scan_tiles_match_oracle(mp, oracle_lib):
         ref = oracle_lib.fluss_arc_count(pi)
         assert np.array_equal(arcs, ref), L
         assert np.array_equal(cac, oracle_lib.fluss_cac(ref, 64)), L
+
+
+def test_fluss_near_arcs_and_tiny_lengths(mp, oracle_lib):
+    """Arcs to the adjacent windows (no interior), to i +- 2 (one interior
+    window, both ends next to each other), self and out-of-range pointers, and
+    lengths 1-3; the near end of every arc is taken in the scan passes and the
+    far end by the atomic pass."""
+    g = np.random.default_rng(45)
+    for L in (1, 2, 3, 5, 4096 + 3):
+        for kind in range(4):
+            i = np.arange(L)
+            off = g.choice([-2, -1, 0, 1, 2], L) if kind == 0 else np.full(L, (-2, 2, 1)[kind - 1])
+            pi = (i + off).astype(np.int64)
+            pi[pi >= L] = -1
+            arcs, cac = mp.fluss(pi, 1)
+            ref = oracle_lib.fluss_arc_count(pi)
+            assert np.array_equal(arcs, ref), (L, kind)
+            assert np.array_equal(cac, oracle_lib.fluss_cac(ref, 1)), (L, kind)
