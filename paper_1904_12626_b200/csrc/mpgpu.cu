@@ -782,6 +782,47 @@ int64_t mpgpu_scrimp_bands(int64_t n, int64_t window, int64_t zone, int64_t s_si
   return take;
 }
 
+namespace {
+// Scratch of the consumer entry points (FLUSS, MASS, extract), kept per
+// (device, kind) across calls: a fresh allocation per call costs more than the
+// work once the memory pool has trimmed it at a synchronisation. Calls of one
+// kind on a device are serialised and each waits on the previous call's use
+// of the buffer.
+enum ScratchKind { kScratchFluss = 0, kScratchMass = 1, kScratchExtract = 2, kScratchKinds = 3 };
+struct Scratch {
+  std::mutex mu;
+  char* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t done = nullptr;
+};
+Scratch g_scratch[64][kScratchKinds];
+
+// Locks the (device, kind) scratch into `lk`, grows it to `need` bytes and
+// orders `st` after its previous use. Pair with scratch_release on `st`.
+mpgpu_status scratch_acquire(int device, int kind, size_t need, cudaStream_t st,
+                             std::unique_lock<std::mutex>& lk, char** out) {
+  if (device < 0 || device >= 64) return fail(MPGPU_EPARAM, "device out of range");
+  Scratch& S = g_scratch[device][kind];
+  lk = std::unique_lock<std::mutex>(S.mu);
+  if (!S.done) MPG_CUDA(cudaEventCreateWithFlags(&S.done, cudaEventDisableTiming));
+  if (S.cap < need) {
+    MPG_CUDA(cudaEventSynchronize(S.done));
+    if (S.p) MPG_CUDA(cudaFree(S.p));
+    S.p = nullptr;
+    S.cap = 0;
+    if (cudaMalloc(&S.p, need) != cudaSuccess) return fail(MPGPU_ENOMEM, "consumer scratch");
+    S.cap = need;
+  }
+  MPG_CUDA(cudaStreamWaitEvent(st, S.done, 0));
+  *out = S.p;
+  return MPGPU_OK;
+}
+mpgpu_status scratch_release(int device, int kind, cudaStream_t st) {
+  MPG_CUDA(cudaEventRecord(g_scratch[device][kind].done, st));
+  return MPGPU_OK;
+}
+}  // namespace
+
 mpgpu_status mpgpu_distance_profiles(const double* d_ts, int64_t n, int64_t window,
                                      const double* d_queries, const int64_t* d_query_pos,
                                      int64_t n_queries, int64_t zone, double* d_out,
@@ -794,13 +835,17 @@ mpgpu_status mpgpu_distance_profiles(const double* d_ts, int64_t n, int64_t wind
   MPG_CUDA(cudaSetDevice(device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const long long L = n - window + 1;
-  double *mu = nullptr, *inv = nullptr;
-  MPG_CUDA(cudaMallocAsync(&mu, sizeof(double) * L, st));
-  MPG_CUDA(cudaMallocAsync(&inv, sizeof(double) * L, st));
+  std::unique_lock<std::mutex> lk;
+  char* scratch = nullptr;
+  if (mpgpu_status e = scratch_acquire(device, kScratchMass,
+                                       sizeof(double) * (2 * L + 3 * n_queries), st, lk, &scratch);
+      e != MPGPU_OK)
+    return e;
+  double* mu = reinterpret_cast<double*>(scratch);
+  double* inv = mu + L;
+  double* qstat = inv + L;
   k_window_stats<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(d_ts, L, (int)window, mu, inv,
                                                               nullptr, nullptr);
-  double* qstat = nullptr;
-  MPG_CUDA(cudaMallocAsync(&qstat, sizeof(double) * 3 * n_queries, st));
   k_query_stats<<<(unsigned)((n_queries + 127) / 128), 128, 0, st>>>(
       d_ts, d_queries, (const long long*)d_query_pos, (int)n_queries, (int)window, qstat);
   dim3 grid((unsigned)((L + kMassTile - 1) / kMassTile), (unsigned)n_queries);
@@ -808,10 +853,7 @@ mpgpu_status mpgpu_distance_profiles(const double* d_ts, int64_t n, int64_t wind
                                         (const long long*)d_query_pos, qstat,
                                         zone < 0 ? -1 : zone, d_out);
   MPG_CUDA(cudaGetLastError());
-  MPG_CUDA(cudaFreeAsync(mu, st));
-  MPG_CUDA(cudaFreeAsync(inv, st));
-  MPG_CUDA(cudaFreeAsync(qstat, st));
-  return MPGPU_OK;
+  return scratch_release(device, kScratchMass, st);
 }
 
 namespace {
@@ -835,19 +877,6 @@ mpgpu_status argext(const double* d_v, long long n, int sign, cudaStream_t st, d
 }
 }  // namespace
 
-namespace {
-// FLUSS scratch (the 32-bit arc-end differences and the tile sums), kept per
-// device across calls: a fresh 4 B/window allocation per call costs more than
-// the whole sweep once the memory pool trims it. Calls on a device are
-// serialised and each waits on the previous call's use of the buffer.
-struct FlussScratch {
-  std::mutex mu;
-  char* p = nullptr;
-  size_t cap = 0;
-  cudaEvent_t done = nullptr;
-};
-FlussScratch g_fluss[64];
-}  // namespace
 
 mpgpu_status mpgpu_fluss(const int64_t* d_index, int64_t L, int64_t window, int64_t* d_arcs,
                          double* d_cac, int32_t device, void* cuda_stream) {
@@ -855,22 +884,13 @@ mpgpu_status mpgpu_fluss(const int64_t* d_index, int64_t L, int64_t window, int6
   MPG_CUDA(cudaSetDevice(device));
   cudaStream_t st = (cudaStream_t)cuda_stream;
   if (L >= (1ll << 31)) return fail(MPGPU_EPARAM, "FLUSS: L must be below 2^31");
-  if (device < 0 || device >= 64) return fail(MPGPU_EPARAM, "device out of range");
   const long long nt = (L + kScanTile - 1) / kScanTile;
-  const size_t need = sizeof(long long) * nt + sizeof(int) * L;
-  FlussScratch& F = g_fluss[device];
-  std::lock_guard<std::mutex> lk(F.mu);
-  if (!F.done) MPG_CUDA(cudaEventCreateWithFlags(&F.done, cudaEventDisableTiming));
-  if (F.cap < need) {
-    MPG_CUDA(cudaEventSynchronize(F.done));
-    if (F.p) MPG_CUDA(cudaFree(F.p));
-    F.p = nullptr;
-    F.cap = 0;
-    if (cudaMalloc(&F.p, need) != cudaSuccess) return fail(MPGPU_ENOMEM, "FLUSS scratch");
-    F.cap = need;
-  }
-  MPG_CUDA(cudaStreamWaitEvent(st, F.done, 0));
-  long long* sums = reinterpret_cast<long long*>(F.p);
+  std::unique_lock<std::mutex> lk;
+  char* scratch = nullptr;
+  if (mpgpu_status e = scratch_acquire(device, kScratchFluss, sizeof(long long) * nt + sizeof(int) * L,
+                                       st, lk, &scratch); e != MPGPU_OK)
+    return e;
+  long long* sums = reinterpret_cast<long long*>(scratch);
   int* diff = reinterpret_cast<int*>(sums + nt);
   MPG_CUDA(cudaMemsetAsync(diff, 0, sizeof(int) * L, st));
   k_arc_far_ends<<<(unsigned)((L + 255) / 256), 256, 0, st>>>((const long long*)d_index, L, diff);
@@ -878,7 +898,7 @@ mpgpu_status mpgpu_fluss(const int64_t* d_index, int64_t L, int64_t window, int6
   k_scan_sums<<<1, 1024, 0, st>>>(sums, nt);
   k_scan_tile_apply<<<(unsigned)nt, kScanThreads, 0, st>>>((const long long*)d_index, diff, L, sums,
                                                            window, (long long*)d_arcs, d_cac);
-  MPG_CUDA(cudaEventRecord(F.done, st));
+  if (mpgpu_status e = scratch_release(device, kScratchFluss, st); e != MPGPU_OK) return e;
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
 }
@@ -889,16 +909,15 @@ int64_t mpgpu_extract(const double* d_values, int64_t n, int64_t k, int64_t zone
   if (!d_values || n < 1 || k < 0 || zone < 0) { fail(MPGPU_EPARAM, "bad extract arguments"); return -1; }
   if (cudaSetDevice(device) != cudaSuccess) { fail(MPGPU_ECUDA, "cudaSetDevice"); return -1; }
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  double* v = nullptr;
-  double* tv = nullptr;
-  long long* ti = nullptr;
   const long long nb = (n + 1023) / 1024;
-  if (cudaMallocAsync(&v, sizeof(double) * n, st) != cudaSuccess ||
-      cudaMallocAsync(&tv, sizeof(double) * 2 * (nb + 2), st) != cudaSuccess ||
-      cudaMallocAsync(&ti, sizeof(long long) * 2 * (nb + 2), st) != cudaSuccess) {
-    fail(MPGPU_ENOMEM, "extract scratch");
+  std::unique_lock<std::mutex> lk;
+  char* scratch = nullptr;
+  if (scratch_acquire(device, kScratchExtract, sizeof(double) * (n + 4 * (nb + 2)), st, lk,
+                      &scratch) != MPGPU_OK)
     return -1;
-  }
+  double* v = reinterpret_cast<double*>(scratch);
+  double* tv = v + n;
+  long long* ti = reinterpret_cast<long long*>(tv + 2 * (nb + 2));
   cudaMemcpyAsync(v, d_values, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
   const int sign = largest ? 1 : -1;
   const double masked = largest ? -INFINITY : INFINITY;  // masked entries are non-finite: skipped
@@ -914,9 +933,7 @@ int64_t mpgpu_extract(const double* d_values, int64_t n, int64_t k, int64_t zone
     const long long span = 2 * zone + 1;
     k_mask_zone<<<(unsigned)((span + 255) / 256), 256, 0, st>>>(v, n, idx, zone, masked);
   }
-  cudaFreeAsync(v, st);
-  cudaFreeAsync(tv, st);
-  cudaFreeAsync(ti, st);
+  scratch_release(device, kScratchExtract, st);
   cudaStreamSynchronize(st);
   return found;
 }
