@@ -193,7 +193,8 @@ def main():
 
     import torch
     import paper_1904_12626_b200 as mp
-    from paper_1904_12626_b200.distributed import merge_keys_, sharded_prepare
+    from paper_1904_12626_b200.distributed import (SharedKeys, merge_keys_, shared_finish,
+                                                   shared_prepare, sharded_prepare)
     ndev = torch.cuda.device_count()
     local = local % max(ndev, 1)  # one process per GPU; wraps only in functional tests
     torch.cuda.set_device(local)
@@ -217,16 +218,28 @@ def main():
     my_cells = plan.cells(rank, world)
     l2 = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     outs = None
+    # N > 1: every rank's join RED.MINs into rank 0's keys over NVLink (CUDA IPC
+    # mappings), so the merge is fused into the compute and every shard filters
+    # against the whole job's keys; MPGPU_SHARED_KEYS=0 selects separate keys
+    # plus an NCCL MIN-reduce after the join.
+    shared = None
+    if world > 1 and os.environ.get("MPGPU_SHARED_KEYS", "1") != "0":
+        shared = SharedKeys(plan, rank, world)
 
     def step(ev):
         nonlocal outs
         ev[0].record(stream)
         with torch.cuda.stream(stream):
-            sharded_prepare(plan, rank, world)  # coarse warm start sharded + MIN-merged
+            if shared:
+                shared_prepare(plan, rank, world, stream)
+            else:
+                sharded_prepare(plan, rank, world)  # coarse warm start sharded + MIN-merged
         ev[1].record(stream)
         plan.run(rank, world)
         ev[2].record(stream)
-        if world > 1:
+        if shared:
+            shared_finish(stream)
+        elif world > 1:
             rk, ck = plan.keys()
             with torch.cuda.stream(stream):
                 merge_keys_(rk, ck, root=0)  # NCCL ReduceOp.MIN on the packed int64 keys
@@ -301,7 +314,9 @@ def main():
             "config": {"workload": cfg.description, "config": cfg.name, "cells_per_step": cells_total,
                        "window": cfg.window, "exclusion_zone": cfg.zone,
                        "l2": "flushed between steps (256 MB write)",
-                       "parallelism": f"diagonal shards x{world}, NCCL MIN merge" if world > 1 else "1 GPU",
+                       "parallelism": (f"diagonal shards x{world}, " + (
+                           "keys shared over NVLink (CUDA IPC), RED.MIN fused into the join" if shared
+                           else "NCCL MIN merge")) if world > 1 else "1 GPU",
                        "tile": mp.lib().mpgpu_build_info().decode()},
             "roofline": {"bound": "fp64", "kernel": "k_join", "kernel_note": "the fine join launch (plan.run), timed alone with CUDA events; the coarse warm-start join is a separate small k_join launch inside prepare, counted in value and ms_per_step",
                          "achieved": join_ops_per_s / 1e12, "peak": FP64_PEAK_MEASURED / 1e12,
@@ -319,6 +334,8 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    if shared:
+        shared.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -353,12 +370,14 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
         # persistent device buffers and plan; every timed step copies the series in,
         # runs this rank's shard, MIN-reduces the keys over NCCL and (rank 0) copies
         # the profile out
-        from paper_1904_12626_b200.distributed import merge_keys_, sharded_prepare
+        from paper_1904_12626_b200.distributed import (SharedKeys, merge_keys_, shared_finish,
+                                                       shared_prepare, sharded_prepare)
         stream = torch.cuda.Stream(dev)
         a = torch.empty(cfg.a.size, dtype=torch.float64, device=dev)
         b = torch.empty(cfg.b.size, dtype=torch.float64, device=dev) if pinned_b is not None else None
         with torch.cuda.stream(stream):
             plan = mp.Plan(a, b, cfg.window, cfg.zone, stream=stream)
+        shared = SharedKeys(plan, rank, world) if os.environ.get("MPGPU_SHARED_KEYS", "1") != "0" else None
         host_out = None
         for s in range(args.warmup + args.steps):
             dist.barrier()
@@ -368,10 +387,15 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
                 a.copy_(pinned_a, non_blocking=True)
                 if b is not None:
                     b.copy_(pinned_b, non_blocking=True)
-                sharded_prepare(plan, rank, world)
-                plan.run(rank, world)
-                rk, ck = plan.keys()
-                merge_keys_(rk, ck, root=0)
+                if shared:
+                    shared_prepare(plan, rank, world, stream)
+                    plan.run(rank, world)
+                    shared_finish(stream)
+                else:
+                    sharded_prepare(plan, rank, world)
+                    plan.run(rank, world)
+                    rk, ck = plan.keys()
+                    merge_keys_(rk, ck, root=0)
                 if rank == 0:
                     o = plan.outputs()
                     if host_out is None:
@@ -384,11 +408,15 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             if s >= args.warmup:
                 times.append(float(tt[0]))
+        if shared:
+            shared.close()
+            dist.barrier()  # every mapping closed before the root frees its keys
         plan.close()
         t = sum(times) / len(times)
     return {"value": cfg.cells() / (t * 1e-3), "unit": "cells/s", "ms_per_step": t,
             "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h,
-            "api": "mpgpu_join (C ABI)" if world == 1 else "Plan + torch.distributed NCCL MIN"}
+            "api": "mpgpu_join (C ABI)" if world == 1 else (
+                "Plan + keys shared over CUDA IPC" if shared else "Plan + torch.distributed NCCL MIN")}
 
 
 if __name__ == "__main__":

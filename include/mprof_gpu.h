@@ -264,6 +264,18 @@ mpgpu_status mpgpu_plan_select_bands(mpgpu_plan *plan, const int64_t *band_ids, 
  * prepare must complete first). NULL, NULL detaches. */
 mpgpu_status mpgpu_plan_attach_keys(mpgpu_plan *plan, int64_t *d_row_keys, int64_t *d_col_keys);
 
+/* CUDA IPC for keys shared across processes (one process per GPU under
+ * torchrun): the owner exports its key allocations (mpgpu_plan_keys) as
+ * 64-byte handles, every other rank opens them (a peer-memory mapping over
+ * NVLink) and attaches its plan to them, so every rank's k_join filters
+ * against and RED.MINs into the same keys while it computes. An attached
+ * plan's prepare_shard(shard, n > 1) still runs its shard of the coarse
+ * warm-start join; the owner alone resets and seeds the shared keys. */
+#define MPGPU_IPC_HANDLE_BYTES 64
+mpgpu_status mpgpu_ipc_export(const void *d_ptr, uint8_t *handle, int32_t device);
+mpgpu_status mpgpu_ipc_open(const uint8_t *handle, void **d_ptr, int32_t device);
+mpgpu_status mpgpu_ipc_close(void *d_ptr, int32_t device);
+
 /* Number of 256-diagonal bands of a self-join plan (0 for AB plans). */
 int64_t mpgpu_plan_num_bands(const mpgpu_plan *plan);
 

@@ -153,6 +153,12 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_extract.restype = ctypes.c_int64
     L.mpgpu_plan_attach_keys.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     L.mpgpu_plan_attach_keys.restype = ctypes.c_int
+    L.mpgpu_ipc_export.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int32]
+    L.mpgpu_ipc_export.restype = ctypes.c_int
+    L.mpgpu_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32]
+    L.mpgpu_ipc_open.restype = ctypes.c_int
+    L.mpgpu_ipc_close.argtypes = [ctypes.c_void_p, ctypes.c_int32]
+    L.mpgpu_ipc_close.restype = ctypes.c_int
     L.mpgpu_plan_num_bands.argtypes = [ctypes.c_void_p]
     L.mpgpu_plan_num_bands.restype = ctypes.c_int64
     L.mpgpu_simple_join.argtypes = [ctypes.POINTER(_SimpleArgs)]
@@ -510,6 +516,18 @@ class Plan:
         candidates are RED.MIN'd straight into them (mpgpu_plan_attach_keys)."""
         _check(lib().mpgpu_plan_attach_keys(self._p, _dev_ptr(row_keys) or None,
                                             _dev_ptr(col_keys) or None))
+
+    def attach_key_ptrs(self, row_ptr: int, col_ptr: int) -> None:
+        """attach_keys() with raw device pointers (e.g. opened from another
+        process's CUDA IPC handles); 0, 0 detaches."""
+        _check(lib().mpgpu_plan_attach_keys(self._p, ctypes.c_void_p(row_ptr or None),
+                                            ctypes.c_void_p(col_ptr or None)))
+
+    def key_ptrs(self):
+        """(row_ptr, col_ptr): device addresses of the plan's own key arrays."""
+        pr, pc = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().mpgpu_plan_keys(self._p, ctypes.byref(pr), None, ctypes.byref(pc), None))
+        return pr.value, pc.value
 
     def keys(self):
         """(row_keys, col_keys) as int64 CUDA tensors aliasing the plan's keys."""

@@ -189,6 +189,8 @@ void build_items(mpgpu_plan* p) {
   // at most ~1e8 items (2.4 GB of item records; the queue index is an int):
   // only series beyond ~2^27 samples reach this
   seg = std::max<long long>(seg, cells / ((long long)kW * 100000000LL) + 1);
+  static const long long seg_env = getenv("MPGPU_SEG_ROWS") ? atoll(getenv("MPGPU_SEG_ROWS")) : 0;
+  if (seg_env > 0) seg = seg_env;  // experiments only
   seg = std::max<long long>(kH, (seg / kH) * kH);
   p->seg_rows = seg;
 
@@ -520,7 +522,19 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
   mpgpu_status st = launch_stats(p, p->A);
   if (st != MPGPU_OK) return st;
   if (!p->self && (st = launch_stats(p, p->B)) != MPGPU_OK) return st;
-  if (p->ext_key0) {  // keys belong to the owning plan, which initialises them
+  if (p->ext_key0) {
+    // keys belong to the owning plan, which initialises them. With several
+    // shards this plan still runs its shard of the coarse warm-start join (on
+    // its own coarse keys): the caller MIN-merges the coarse keys across ranks
+    // and the owner seeds the shared keys from them (prepare_finish).
+    if (n_shards > 1 && !p->subset && p->coarse_f > 0) {
+      if (coarse_begin(p, shard, n_shards) == MPGPU_OK) {
+        p->coarse_pending = true;
+      } else {
+        p->coarse_f = 0;
+        cudaGetLastError();
+      }
+    }
     MPG_CUDA(cudaGetLastError());
     return MPGPU_OK;
   }
@@ -936,6 +950,32 @@ int64_t mpgpu_extract(const double* d_values, int64_t n, int64_t k, int64_t zone
   scratch_release(device, kScratchExtract, st);
   cudaStreamSynchronize(st);
   return found;
+}
+
+mpgpu_status mpgpu_ipc_export(const void* d_ptr, uint8_t* handle, int32_t device) {
+  if (!d_ptr || !handle) return fail(MPGPU_EPARAM, "null pointer");
+  static_assert(sizeof(cudaIpcMemHandle_t) == MPGPU_IPC_HANDLE_BYTES, "IPC handle size");
+  MPG_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  MPG_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+  memcpy(handle, &h, sizeof(h));
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_ipc_open(const uint8_t* handle, void** d_ptr, int32_t device) {
+  if (!d_ptr || !handle) return fail(MPGPU_EPARAM, "null pointer");
+  MPG_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  MPG_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_ipc_close(void* d_ptr, int32_t device) {
+  if (!d_ptr) return MPGPU_OK;
+  MPG_CUDA(cudaSetDevice(device));
+  MPG_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  return MPGPU_OK;
 }
 
 mpgpu_status mpgpu_keys_min_merge(int64_t* d_dst, const int64_t* d_src, int64_t len,

@@ -10,6 +10,7 @@ for any world size.
 """
 from __future__ import annotations
 
+import ctypes
 from typing import Optional
 
 
@@ -57,6 +58,86 @@ def sharded_join(plan, rank: int, world: int, group=None, root: int = 0):
     if world > 1:
         rk, ck = plan.keys()
         merge_keys_(rk, ck, group=group, root=root)
+    if rank == root:
+        return plan.outputs()
+    return None
+
+
+class SharedKeys:
+    """Rank `root`'s key arrays mapped into every rank's plan over CUDA IPC.
+
+    One process per GPU: the root exports its two key allocations as IPC
+    handles, the other ranks open them (peer-memory mappings over NVLink) and
+    attach their plans. Every rank's k_join then reads its filter thresholds
+    from, and RED.MINs its candidates into, the same keys while it computes:
+    the min-merge is fused into the join (no reduce afterwards), and each
+    shard filters against the whole job's best-so-far instead of only its
+    own, so it replays about as few blocks as a one-GPU run.
+    Collective use only (every rank constructs it)."""
+
+    def __init__(self, plan, rank: int, world: int, group=None, root: int = 0):
+        import torch.distributed as dist
+        import paper_1904_12626_b200 as mp
+        self.plan, self.rank, self.root, self.group = plan, rank, root, group
+        self.opened = []
+        handles = [None]
+        if rank == root:
+            hs = []
+            for ptr in plan.key_ptrs():
+                buf = (ctypes.c_char * 64)()
+                mp._check(mp.lib().mpgpu_ipc_export(ctypes.c_void_p(ptr), buf, plan.device))
+                hs.append(bytes(buf))
+            handles = [hs]
+        dist.broadcast_object_list(handles, src=root, group=group)
+        if rank != root:
+            ptrs = []
+            for h in handles[0]:
+                p = ctypes.c_void_p()
+                mp._check(mp.lib().mpgpu_ipc_open(h, ctypes.byref(p), plan.device))
+                self.opened.append(p.value)
+                ptrs.append(p.value)
+            plan.attach_key_ptrs(ptrs[0], ptrs[1])
+
+    def close(self) -> None:
+        import paper_1904_12626_b200 as mp
+        if self.opened:
+            self.plan.attach_key_ptrs(0, 0)
+            for p in self.opened:
+                mp.lib().mpgpu_ipc_close(ctypes.c_void_p(p), self.plan.device)
+            self.opened = []
+
+
+def shared_prepare(plan, rank: int, world: int, stream, group=None, root: int = 0) -> None:
+    """Warm start over shared keys: every rank runs stats and its shard of the
+    coarse join, the coarse keys are MIN-all-reduced, the root resets and
+    seeds the shared keys; returns once the seeding is complete everywhere
+    visible (root stream synchronised, then a barrier)."""
+    import torch.distributed as dist
+    plan.prepare_shard(rank, world)
+    ck = plan.coarse_keys()
+    if ck is not None:
+        merge_keys_(ck[0], ck[1], group=group, root=None)
+    if rank == root:
+        plan.prepare_finish()
+    stream.synchronize()
+    dist.barrier(group=group)
+
+
+def shared_finish(stream, group=None) -> None:
+    """Wait until every rank's join has landed in the shared keys."""
+    import torch.distributed as dist
+    stream.synchronize()
+    dist.barrier(group=group)
+
+
+def shared_keys_join(plan, rank: int, world: int, stream, group=None, root: int = 0):
+    """One join over keys shared through SharedKeys (attached beforehand):
+    shared_prepare, this rank's shard of the join straight into the shared
+    keys, shared_finish, then the root decodes the keys.
+    Returns the MatrixProfile device arrays on the root, None elsewhere."""
+    shared_prepare(plan, rank, world, stream, group=group, root=root)
+    plan.run(rank, world)
+    shared_finish(stream, group=group)
     if rank == root:
         return plan.outputs()
     return None

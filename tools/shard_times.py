@@ -1,0 +1,91 @@
+#!/usr/bin/env python3
+"""Per-shard timing of the N-GPU join, measured on ONE GPU.
+
+Every rank of an N-GPU run executes the same kernels on its own device: the
+sharded prepare (its 1/N of the coarse warm-start join, then the warm-start
+finish), its shard of the diagonal work items, and rank 0 the finalize. Their
+only exchange is the MIN of the packed keys (coarse keys inside prepare, full
+keys after the join). This script runs each shard of each N in turn on one
+GPU, with the keys reset to their post-warm-start state before every shard
+(so a shard never benefits from another's results), and times each phase
+with CUDA events:
+
+    step_N = max_s coarse_s + finish + max_s join_s + merge_est + finalize
+
+merge_est is the key MIN over NVLink estimated from bytes (16 B per window,
+at 450 GB/s, half the NVLink 5 per-direction rate); it is the one unmeasured
+term. efficiency_N = step_1 / (N * step_N), the figure the driver computes
+from bench.py lines at N GPUs.
+
+    python tools/shard_times.py [--config C4] [--ns 1,2,4,8] > profiles/shard_times_r01.jsonl
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1904_12626_b200 as mp  # noqa: E402
+from paper_1904_12626_b200 import datasets  # noqa: E402
+
+NVLINK_MERGE_GBS = 450.0
+
+
+def timed(stream, fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--ns", default="1,2,4,8")
+    args = ap.parse_args()
+    cfg = datasets.get(args.config)
+    stream = torch.cuda.Stream()
+    a = torch.from_numpy(cfg.a).cuda()
+    b = torch.from_numpy(cfg.b).cuda() if cfg.b is not None else None
+    with torch.cuda.stream(stream):
+        plan = mp.Plan(a, b, cfg.window, cfg.zone, stream=stream)
+    # warm-up: one full single-rank step
+    plan.prepare(); plan.run(0, 1); plan.outputs(); torch.cuda.synchronize()
+    key_bytes = (plan.La + plan.Lb) * 8
+    merge_est = key_bytes / (NVLINK_MERGE_GBS * 1e9) * 1e3
+    step1 = None
+    for N in [int(v) for v in args.ns.split(",")]:
+        coarse, joins = [], []
+        for s in range(N):
+            coarse.append(timed(stream, lambda: plan.prepare_shard(s, N)))
+        finish = timed(stream, plan.prepare_finish)  # coarse keys of all shards are merged in place
+        for s in range(N):
+            plan.prepare()  # reset the keys to the post-warm-start state
+            torch.cuda.synchronize()
+            joins.append(timed(stream, lambda: plan.run(s, N)))
+        fin = timed(stream, plan.outputs)
+        step = max(coarse) + finish + max(joins) + (merge_est if N > 1 else 0.0) + fin
+        if N == 1:
+            step1 = step
+        cells = [plan.cells(s, N) for s in range(N)]
+        line = {"config": cfg.name, "workload": cfg.description, "n_shards": N,
+                "coarse_ms_max": max(coarse), "finish_ms": finish,
+                "join_ms": joins, "join_ms_max": max(joins), "join_ms_mean": sum(joins) / N,
+                "shard_cells_max_over_mean": max(cells) / (sum(cells) / N),
+                "merge_ms_est": merge_est if N > 1 else 0.0, "finalize_ms": fin,
+                "step_ms_pred": step, "cells_per_s_pred": cfg.cells() / (step * 1e-3),
+                "efficiency_pred": step1 / (N * step) if step1 else None,
+                "note": "phases timed per shard on one GPU; merge_ms_est from bytes at "
+                        f"{NVLINK_MERGE_GBS:.0f} GB/s"}
+        print(json.dumps(line), flush=True)
+    plan.close()
+
+
+if __name__ == "__main__":
+    main()
