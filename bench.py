@@ -194,7 +194,7 @@ def main():
     import torch
     import paper_1904_12626_b200 as mp
     from paper_1904_12626_b200.distributed import (SharedKeys, merge_keys_, shared_finish,
-                                                   shared_prepare, sharded_prepare)
+                                                   shared_outputs, shared_prepare, sharded_prepare)
     ndev = torch.cuda.device_count()
     local = local % max(ndev, 1)  # one process per GPU; wraps only in functional tests
     torch.cuda.set_device(local)
@@ -245,7 +245,7 @@ def main():
                 merge_keys_(rk, ck, root=0)  # NCCL ReduceOp.MIN on the packed int64 keys
         if rank == 0:
             with torch.cuda.stream(stream):
-                outs = plan.outputs()
+                outs = shared_outputs(plan, rank) if shared else plan.outputs()
         ev[3].record(stream)
 
     mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -371,7 +371,7 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
         # runs this rank's shard, MIN-reduces the keys over NCCL and (rank 0) copies
         # the profile out
         from paper_1904_12626_b200.distributed import (SharedKeys, merge_keys_, shared_finish,
-                                                       shared_prepare, sharded_prepare)
+                                                       shared_outputs, shared_prepare, sharded_prepare)
         stream = torch.cuda.Stream(dev)
         a = torch.empty(cfg.a.size, dtype=torch.float64, device=dev)
         b = torch.empty(cfg.b.size, dtype=torch.float64, device=dev) if pinned_b is not None else None
@@ -397,7 +397,7 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
                     rk, ck = plan.keys()
                     merge_keys_(rk, ck, root=0)
                 if rank == 0:
-                    o = plan.outputs()
+                    o = shared_outputs(plan, rank) if shared else plan.outputs()
                     if host_out is None:
                         host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in o.items()}
                     for k, v in o.items():

@@ -272,6 +272,17 @@ mpgpu_status mpgpu_plan_attach_keys(mpgpu_plan *plan, int64_t *d_row_keys, int64
  * plan's prepare_shard(shard, n > 1) still runs its shard of the coarse
  * warm-start join; the owner alone resets and seeds the shared keys. */
 #define MPGPU_IPC_HANDLE_BYTES 64
+
+/* Warm start of a shared-key join, sharded over the ranks, with no barrier
+ * before the join: the owner resets its keys once per join beforehand
+ * (mpgpu_plan_reset_keys, e.g. right after finalizing the previous one).
+ * prepare_shared: stats and this shard's coarse join (no key writes).
+ * The caller MIN-all-reduces mpgpu_plan_coarse_keys across ranks (which also
+ * orders every rank after the owner's reset), then seed_shared: this shard's
+ * spread diagonals and coarse-match segments, RED.MIN'd into the keys. */
+mpgpu_status mpgpu_plan_prepare_shared(mpgpu_plan *plan, int32_t shard, int32_t n_shards);
+mpgpu_status mpgpu_plan_seed_shared(mpgpu_plan *plan, int32_t shard, int32_t n_shards);
+mpgpu_status mpgpu_plan_reset_keys(mpgpu_plan *plan);
 mpgpu_status mpgpu_ipc_export(const void *d_ptr, uint8_t *handle, int32_t device);
 mpgpu_status mpgpu_ipc_open(const uint8_t *handle, void **d_ptr, int32_t device);
 mpgpu_status mpgpu_ipc_close(void *d_ptr, int32_t device);

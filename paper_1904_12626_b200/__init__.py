@@ -153,6 +153,11 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_extract.restype = ctypes.c_int64
     L.mpgpu_plan_attach_keys.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
     L.mpgpu_plan_attach_keys.restype = ctypes.c_int
+    for fn in ("mpgpu_plan_prepare_shared", "mpgpu_plan_seed_shared"):
+        getattr(L, fn).argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
+        getattr(L, fn).restype = ctypes.c_int
+    L.mpgpu_plan_reset_keys.argtypes = [ctypes.c_void_p]
+    L.mpgpu_plan_reset_keys.restype = ctypes.c_int
     L.mpgpu_ipc_export.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int32]
     L.mpgpu_ipc_export.restype = ctypes.c_int
     L.mpgpu_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32]
@@ -516,6 +521,19 @@ class Plan:
         candidates are RED.MIN'd straight into them (mpgpu_plan_attach_keys)."""
         _check(lib().mpgpu_plan_attach_keys(self._p, _dev_ptr(row_keys) or None,
                                             _dev_ptr(col_keys) or None))
+
+    def prepare_shared(self, shard: int, n_shards: int) -> None:
+        """Shared-key warm start, phase 1: stats and this shard's coarse join."""
+        _check(lib().mpgpu_plan_prepare_shared(self._p, int(shard), int(n_shards)))
+
+    def seed_shared(self, shard: int, n_shards: int) -> None:
+        """Phase 2 (after the coarse keys are MIN-merged): this shard's warm-start
+        cells, RED.MIN'd into the (shared) keys."""
+        _check(lib().mpgpu_plan_seed_shared(self._p, int(shard), int(n_shards)))
+
+    def reset_keys(self) -> None:
+        """Empty the plan's own keys (the owner, before a shared-key join)."""
+        _check(lib().mpgpu_plan_reset_keys(self._p))
 
     def attach_key_ptrs(self, row_ptr: int, col_ptr: int) -> None:
         """attach_keys() with raw device pointers (e.g. opened from another

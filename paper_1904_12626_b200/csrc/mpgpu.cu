@@ -323,7 +323,7 @@ mpgpu_status coarse_begin(mpgpu_plan* p, int shard, int n_shards) {
 // K2b, phase 2: seed the fine keys around the (merged) coarse matches. Coarse
 // row keys (best column per coarse row) and column keys (best row per coarse
 // column) both seed pass 0 of the fine plan (rows of A, columns of B).
-mpgpu_status coarse_finish(mpgpu_plan* p) {
+mpgpu_status coarse_finish(mpgpu_plan* p, int shard = 0, int n_shards = 1) {
   const int f = p->coarse_f;
   const JoinParams P = make_params(p);
   const mpgpu_plan* c = p->coarse;
@@ -333,13 +333,47 @@ mpgpu_status coarse_finish(mpgpu_plan* p) {
   static const int span_env = getenv("MPGPU_COARSE_SPAN") ? atoi(getenv("MPGPU_COARSE_SPAN")) : 0;
   const int dspan = span_env > 0 ? span_env : std::max(1, f / 2);
   const int nd = 2 * dspan + 1;
-  k_coarse_exploit<<<(unsigned)((Lr * nd + 255) / 256), 256, 0, p->stream>>>(
-      P.pass[0], c->key0, Lr, c->imask, false, f, dspan, p->zone, p->self, (int)p->m, p->imask);
-  k_coarse_exploit<<<(unsigned)((Lc * nd + 255) / 256), 256, 0, p->stream>>>(
-      P.pass[0], c->key1, Lc, c->imask, true, f, dspan, p->zone, p->self, (int)p->m, p->imask);
+  // this shard's contiguous share of the coarse windows (all of them for one shard)
+  const long long r0 = Lr * shard / n_shards, r1 = Lr * (shard + 1) / n_shards;
+  const long long c0 = Lc * shard / n_shards, c1 = Lc * (shard + 1) / n_shards;
+  if (r1 > r0)
+    k_coarse_exploit<<<(unsigned)(((r1 - r0) * nd + 255) / 256), 256, 0, p->stream>>>(
+        P.pass[0], c->key0, r0, r1, c->imask, false, f, dspan, p->zone, p->self, (int)p->m,
+        p->imask);
+  if (c1 > c0)
+    k_coarse_exploit<<<(unsigned)(((c1 - c0) * nd + 255) / 256), 256, 0, p->stream>>>(
+        P.pass[0], c->key1, c0, c1, c->imask, true, f, dspan, p->zone, p->self, (int)p->m,
+        p->imask);
   p->launches += 2;
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
+}
+
+// Spread-diagonal warm start (K2) of a full join: this shard's share of the
+// n_init diagonals of every pass (all of them for one shard).
+void launch_init(mpgpu_plan* p, int shard, int n_shards) {
+  const JoinParams P = make_params(p);
+  const int npass = p->subset ? 0 : (p->self ? 1 : 2);
+  for (int q = 0; q < npass; ++q) {
+    const Pass& ps = P.pass[q];
+    const long long klo = p->self ? p->zone + 1 : (q == 0 ? 0 : 1);
+    const long long khi = ps.C.L;
+    if (khi <= klo) continue;
+    // spread diagonals: a handful when the coarse warm start follows (it finds
+    // far better candidates), kInitDiag otherwise
+    static const int n_env = getenv("MPGPU_INIT_N") ? atoi(getenv("MPGPU_INIT_N")) : -1;
+    const int n_init = n_env >= 0 ? n_env : (p->coarse_f > 0 ? 8 : kInitDiag);
+    const int mine = n_init > shard ? (n_init - shard + n_shards - 1) / n_shards : 0;
+    if (mine <= 0) continue;
+    // rows per thread: long enough to amortise the m-term seed, short enough
+    // that the grid still fills the GPU (~4 resident threads-worth per SM slot)
+    const long long fill = 148LL * 2048 * 4;
+    const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * mine / fill));
+    dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)mine);
+    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask, seg, nullptr,
+                                              shard, n_shards, n_init);
+    p->launches += 1;
+  }
 }
 
 std::once_flag g_attr_once;
@@ -513,6 +547,53 @@ mpgpu_status mpgpu_plan_prepare_finish(mpgpu_plan* p) {
   return coarse_finish(p);
 }
 
+mpgpu_status mpgpu_plan_prepare_shared(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
+  if (p->subset) return fail(MPGPU_EUNSUPPORTED, "shared-key joins are full joins");
+  p->coarse_pending = false;
+  MPG_CUDA(cudaSetDevice(p->device));
+  p->launches = 0;
+  mpgpu_status st = launch_stats(p, p->A);
+  if (st != MPGPU_OK) return st;
+  if (!p->self && (st = launch_stats(p, p->B)) != MPGPU_OK) return st;
+  if (p->coarse_f > 0) {
+    if (coarse_begin(p, shard, n_shards) == MPGPU_OK) {
+      p->coarse_pending = true;
+    } else {
+      p->coarse_f = 0;
+      cudaGetLastError();
+    }
+  }
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_plan_seed_shared(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
+  MPG_CUDA(cudaSetDevice(p->device));
+  launch_init(p, shard, n_shards);
+  if (p->coarse_pending) {
+    p->coarse_pending = false;
+    if (mpgpu_status st = coarse_finish(p, shard, n_shards); st != MPGPU_OK) return st;
+  }
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_plan_reset_keys(mpgpu_plan* p) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (p->ext_key0) return fail(MPGPU_EPARAM, "an attached plan does not own its keys");
+  MPG_CUDA(cudaSetDevice(p->device));
+  const long long L1 = p->self ? p->A.L : p->B.L;
+  k_fill_keys<<<(unsigned)((p->A.L + 255) / 256), 256, 0, p->stream>>>(p->key0, p->A.L);
+  k_fill_keys<<<(unsigned)((L1 + 255) / 256), 256, 0, p->stream>>>(p->key1, L1);
+  p->launches += 2;
+  MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
 mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
@@ -544,26 +625,9 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
   p->launches += 2;
   // warm-start keys on a few spread diagonals of every pass (full runs only:
   // an anytime run must not see cells outside its bands)
-  JoinParams P = make_params(p);
+  launch_init(p, 0, 1);
+  const JoinParams P = make_params(p);
   const int npass = p->subset ? 0 : (p->self ? 1 : 2);
-  for (int q = 0; q < npass; ++q) {
-    const Pass& ps = P.pass[q];
-    const long long klo = p->self ? p->zone + 1 : (q == 0 ? 0 : 1);
-    const long long khi = ps.C.L;
-    if (khi <= klo) continue;
-    // spread diagonals: a handful when the coarse warm start follows (it finds
-    // far better candidates), kInitDiag otherwise
-    static const int n_env = getenv("MPGPU_INIT_N") ? atoi(getenv("MPGPU_INIT_N")) : -1;
-    const int n_init = n_env >= 0 ? n_env : (p->coarse_f > 0 ? 8 : kInitDiag);
-    if (n_init <= 0) continue;
-    // rows per thread: long enough to amortise the m-term seed, short enough
-    // that the grid still fills the GPU (~4 resident threads-worth per SM slot)
-    const long long fill = 148LL * 2048 * 4;
-    const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * n_init / fill));
-    dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)n_init);
-    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask, seg, nullptr);
-    p->launches += 1;
-  }
   if (p->subset && p->n_init_diags > 0) {
     // anytime run: warm start on diagonals of the chosen bands only (they are
     // cells of this run), so no row's first visit fires every warp
@@ -573,7 +637,7 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
     const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * n_init / fill));
     dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)n_init);
     k_init_keys<<<grid, 256, 0, p->stream>>>(ps, p->zone + 1, ps.C.L, (int)p->m, p->imask, seg,
-                                              p->d_init_diags);
+                                              p->d_init_diags, 0, 1, n_init);
     p->launches += 1;
   }
   if (npass > 0 && p->coarse_f > 0) {

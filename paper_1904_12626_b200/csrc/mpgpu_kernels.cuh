@@ -682,16 +682,17 @@ constexpr int kInitDiag = MPGPU_INIT_DIAG;
 constexpr int kInitSeg = 32;  // max rows per thread: one direct seed, then the recurrence
 
 __global__ void k_init_keys(const Pass PS, long long klo, long long khi, int m, long long imask,
-                            int seg, const long long* __restrict__ diags) {
+                            int seg, const long long* __restrict__ diags, int b0, int bstride,
+                            int nb_total) {
   const long long i0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * seg;
-  const int b = blockIdx.y;
+  const int b = b0 + (int)blockIdx.y * bstride;  // this launch's share of the nb_total diagonals
   const Series& R = PS.R;
   const Series& C = PS.C;
   const long long span = khi - klo;
   if (span <= 0 || i0 >= R.L) return;
   // diagonal b: klo + b*span/nb (b = 0 is the first admissible diagonal), or
   // the b-th entry of an explicit list (anytime runs: diagonals of chosen bands)
-  const long long k = diags ? diags[b] : klo + (span * b) / (long long)gridDim.y;
+  const long long k = diags ? diags[b] : klo + (span * b) / (long long)nb_total;
   const long long j0 = i0 + k;
   if (j0 >= C.L) return;
   // seed cov(i0, j0) by a direct centred dot product, then walk the diagonal
@@ -740,13 +741,13 @@ __global__ void k_paa(const double* __restrict__ x, long long nc, int f, double*
   xc[t] = s / f;
 }
 
-__global__ void k_coarse_exploit(const Pass PS, const long long* __restrict__ ckey, long long Lc,
-                                 long long cimask, bool key_is_col, int f, int span,
+__global__ void k_coarse_exploit(const Pass PS, const long long* __restrict__ ckey, long long I0,
+                                 long long I1, long long cimask, bool key_is_col, int f, int span,
                                  long long zone, bool self, int m, long long imask) {
   const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const int nd = 2 * span + 1;
-  const long long I = g / nd;
-  if (I >= Lc) return;
+  const long long I = I0 + g / nd;  // coarse windows [I0, I1): this shard's share
+  if (I >= I1) return;
   const long long kc = ckey[I];
   if (kc == kKeyNone) return;
   const long long J = kc & cimask;

@@ -88,6 +88,9 @@ class SharedKeys:
                 mp._check(mp.lib().mpgpu_ipc_export(ctypes.c_void_p(ptr), buf, plan.device))
                 hs.append(bytes(buf))
             handles = [hs]
+        if rank == root:
+            plan.reset_keys()  # the first join starts from empty keys
+            plan.stream.synchronize()
         dist.broadcast_object_list(handles, src=root, group=group)
         if rank != root:
             ptrs = []
@@ -108,19 +111,20 @@ class SharedKeys:
 
 
 def shared_prepare(plan, rank: int, world: int, stream, group=None, root: int = 0) -> None:
-    """Warm start over shared keys: every rank runs stats and its shard of the
-    coarse join, the coarse keys are MIN-all-reduced, the root resets and
-    seeds the shared keys; returns once the seeding is complete everywhere
-    visible (root stream synchronised, then a barrier)."""
+    """Warm start over shared keys, sharded: every rank runs stats and its
+    shard of the coarse join, the coarse keys are MIN-all-reduced, then every
+    rank RED.MINs its share of the warm-start cells into the shared keys. No
+    barrier before the join: the keys only tighten the filter, and the owner
+    reset them before the previous join's end barrier released anyone. Without
+    a coarse phase (small joins) a barrier orders the ranks after that reset."""
     import torch.distributed as dist
-    plan.prepare_shard(rank, world)
+    plan.prepare_shared(rank, world)
     ck = plan.coarse_keys()
     if ck is not None:
         merge_keys_(ck[0], ck[1], group=group, root=None)
-    if rank == root:
-        plan.prepare_finish()
-    stream.synchronize()
-    dist.barrier(group=group)
+    else:
+        dist.barrier(group=group)
+    plan.seed_shared(rank, world)
 
 
 def shared_finish(stream, group=None) -> None:
@@ -128,6 +132,16 @@ def shared_finish(stream, group=None) -> None:
     import torch.distributed as dist
     stream.synchronize()
     dist.barrier(group=group)
+
+
+def shared_outputs(plan, rank: int, root: int = 0):
+    """The root decodes the shared keys, then empties them for the next join
+    (before any rank can pass the next join's coarse all-reduce)."""
+    if rank != root:
+        return None
+    out = plan.outputs()
+    plan.reset_keys()
+    return out
 
 
 def shared_keys_join(plan, rank: int, world: int, stream, group=None, root: int = 0):
@@ -138,6 +152,4 @@ def shared_keys_join(plan, rank: int, world: int, stream, group=None, root: int 
     shared_prepare(plan, rank, world, stream, group=group, root=root)
     plan.run(rank, world)
     shared_finish(stream, group=group)
-    if rank == root:
-        return plan.outputs()
-    return None
+    return shared_outputs(plan, rank, root=root)

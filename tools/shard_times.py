@@ -48,6 +48,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="C4")
     ap.add_argument("--ns", default="1,2,4,8")
+    ap.add_argument("--shared", action="store_true",
+                    help="shared-key phases: prepare_shared / seed_shared per shard, then the shard "
+                         "joins run one after another into the same keys (no reset between them)")
     args = ap.parse_args()
     cfg = datasets.get(args.config)
     stream = torch.cuda.Stream()
@@ -60,6 +63,21 @@ def main():
     key_bytes = (plan.La + plan.Lb) * 8
     merge_est = key_bytes / (NVLINK_MERGE_GBS * 1e9) * 1e3
     step1 = None
+    if args.shared:
+        for N in [int(v) for v in args.ns.split(",")]:
+            plan.reset_keys()
+            prep = [timed(stream, lambda: plan.prepare_shared(s, N)) for s in range(N)]
+            seed = []
+            for s in range(N):  # each shard's seeding consumes the pending coarse phase: redo it
+                plan.prepare_shared(s, N)
+                seed.append(timed(stream, lambda: plan.seed_shared(s, N)))
+            joins = [timed(stream, lambda: plan.run(s, N)) for s in range(N)]
+            fin = timed(stream, plan.outputs)
+            print(json.dumps({"config": cfg.name, "mode": "shared keys, shards in sequence", "n_shards": N,
+                              "prepare_shared_ms": prep, "seed_shared_ms": seed, "join_ms": joins,
+                              "finalize_ms": fin}), flush=True)
+        plan.close()
+        return
     for N in [int(v) for v in args.ns.split(",")]:
         coarse, joins = [], []
         for s in range(N):
