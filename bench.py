@@ -224,7 +224,7 @@ def main():
     # plus an NCCL MIN-reduce after the join.
     shared = None
     if world > 1 and os.environ.get("MPGPU_SHARED_KEYS", "1") != "0":
-        shared = SharedKeys(plan, rank, world)
+        shared = SharedKeys.try_create(plan, rank, world)
 
     def step(ev):
         nonlocal outs
@@ -377,7 +377,8 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
         b = torch.empty(cfg.b.size, dtype=torch.float64, device=dev) if pinned_b is not None else None
         with torch.cuda.stream(stream):
             plan = mp.Plan(a, b, cfg.window, cfg.zone, stream=stream)
-        shared = SharedKeys(plan, rank, world) if os.environ.get("MPGPU_SHARED_KEYS", "1") != "0" else None
+        shared = (SharedKeys.try_create(plan, rank, world)
+                  if os.environ.get("MPGPU_SHARED_KEYS", "1") != "0" else None)
         host_out = None
         for s in range(args.warmup + args.steps):
             dist.barrier()

@@ -82,16 +82,20 @@ class SharedKeys:
         self.opened = []
         handles = [None]
         if rank == root:
-            hs = []
-            for ptr in plan.key_ptrs():
-                buf = (ctypes.c_char * 64)()
-                mp._check(mp.lib().mpgpu_ipc_export(ctypes.c_void_p(ptr), buf, plan.device))
-                hs.append(bytes(buf))
-            handles = [hs]
-        if rank == root:
-            plan.reset_keys()  # the first join starts from empty keys
-            plan.stream.synchronize()
+            try:
+                hs = []
+                for ptr in plan.key_ptrs():
+                    buf = (ctypes.c_char * 64)()
+                    mp._check(mp.lib().mpgpu_ipc_export(ctypes.c_void_p(ptr), buf, plan.device))
+                    hs.append(bytes(buf))
+                plan.reset_keys()  # the first join starts from empty keys
+                plan.stream.synchronize()
+                handles = [hs]
+            except Exception as e:  # noqa: BLE001 -- tell the other ranks before raising
+                handles = [f"export failed: {e}"]
         dist.broadcast_object_list(handles, src=root, group=group)
+        if isinstance(handles[0], str):
+            raise RuntimeError(handles[0])
         if rank != root:
             ptrs = []
             for h in handles[0]:
@@ -100,6 +104,30 @@ class SharedKeys:
                 self.opened.append(p.value)
                 ptrs.append(p.value)
             plan.attach_key_ptrs(ptrs[0], ptrs[1])
+
+    @classmethod
+    def try_create(cls, plan, rank: int, world: int, group=None, root: int = 0):
+        """SharedKeys, or None on every rank when any rank cannot map the keys
+        (e.g. no peer access between its GPU and the root's): the caller then
+        keeps separate keys and MIN-reduces them after the join."""
+        import sys
+        import torch
+        import torch.distributed as dist
+        sk, ok = None, 1
+        try:
+            sk = cls(plan, rank, world, group=group, root=root)
+        except Exception as e:  # noqa: BLE001 -- reported, then agreed on collectively
+            ok = 0
+            print(f"[mprof_b200] rank {rank}: shared keys unavailable ({e}); using the NCCL merge",
+                  file=sys.stderr)
+        flag = torch.tensor([ok], dtype=torch.int32,
+                            device=plan.a.device if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()) == 0:
+            if sk is not None:
+                sk.close()
+            return None
+        return sk
 
     def close(self) -> None:
         import paper_1904_12626_b200 as mp
