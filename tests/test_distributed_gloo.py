@@ -107,3 +107,46 @@ def test_world_size_invariance_model():
         row = np.minimum.reduce([p[0] for p in parts])
         col = np.minimum.reduce([p[1] for p in parts])
         assert np.array_equal(row, base[0]) and np.array_equal(col, base[1])
+
+
+class _FakePlan:
+    """Stands in for a Plan whose keys cannot be exported (no device here):
+    the C ABI's mpgpu_ipc_export fails and SharedKeys must not leave the
+    other ranks waiting."""
+
+    device = 0
+
+    class a:  # noqa: N801 -- mirrors Plan.a.device
+        device = torch.device("cpu")
+
+    def key_ptrs(self):
+        return 4096, 8192
+
+    def reset_keys(self):
+        raise AssertionError("not reached: the export fails first")
+
+
+def _fallback_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sk = distributed.SharedKeys.try_create(_FakePlan(), rank, world)
+    out_q.put((rank, sk is None))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shared_keys_fall_back_together_when_export_fails():
+    """Every rank gets None (and so keeps the NCCL merge) when the root cannot
+    export its keys; nobody hangs in the handle broadcast."""
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fallback_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == {0: True, 1: True}
