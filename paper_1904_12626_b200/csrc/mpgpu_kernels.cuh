@@ -250,8 +250,9 @@ struct __align__(16) JoinSmem {
   WarpSmem w[kWarps];
 };
 
+// x < 2^31 (segment-local column offsets): 32-bit modulo, not a 64-bit one
 __device__ __forceinline__ int ring_addr(long long x) {
-  const int p = (int)(x % kRing);
+  const int p = (int)((unsigned)x % (unsigned)kRing);
   return (p % kD) * kNB + p / kD;
 }
 
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       // schedule freely across earlier ones. A block in which any lane fired
       // (a few percent) is replayed from its saved start state with the
       // per-row-step slow path; the arithmetic of every cell is identical.
-      int b0 = (int)((ts / kD + lane) % kNB);
+      int b0 = (int)(((unsigned)ts / kD + lane) % (unsigned)kNB);
       for (int u = 0; u < kH; u += kD) {
         const int b1 = b0 + 1 == kNB ? 0 : b0 + 1;
 #pragma unroll
