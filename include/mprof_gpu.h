@@ -283,6 +283,16 @@ mpgpu_status mpgpu_plan_attach_keys(mpgpu_plan *plan, int64_t *d_row_keys, int64
 mpgpu_status mpgpu_plan_prepare_shared(mpgpu_plan *plan, int32_t shard, int32_t n_shards);
 mpgpu_status mpgpu_plan_seed_shared(mpgpu_plan *plan, int32_t shard, int32_t n_shards);
 mpgpu_status mpgpu_plan_reset_keys(mpgpu_plan *plan);
+
+/* Coarse warm-start keys shared the same way (they would otherwise see only
+ * each rank's own coarse shard): the owner takes the nested coarse plan's key
+ * arrays (NULL when the plan has no coarse phase) and exports them, the other
+ * ranks attach. prepare_shared then stops before the coarse join, and every
+ * rank runs its coarse shard with coarse_run once the owner's prepare_shared
+ * is complete (a barrier), then seed_shared once every coarse_run is. */
+mpgpu_status mpgpu_plan_coarse_key_ptrs(mpgpu_plan *plan, int64_t **d_row_keys, int64_t **d_col_keys);
+mpgpu_status mpgpu_plan_attach_coarse_keys(mpgpu_plan *plan, int64_t *d_row_keys, int64_t *d_col_keys);
+mpgpu_status mpgpu_plan_coarse_run(mpgpu_plan *plan, int32_t shard, int32_t n_shards);
 mpgpu_status mpgpu_ipc_export(const void *d_ptr, uint8_t *handle, int32_t device);
 mpgpu_status mpgpu_ipc_open(const uint8_t *handle, void **d_ptr, int32_t device);
 mpgpu_status mpgpu_ipc_close(void *d_ptr, int32_t device);

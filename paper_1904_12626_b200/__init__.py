@@ -156,6 +156,13 @@ def lib() -> ctypes.CDLL:
     for fn in ("mpgpu_plan_prepare_shared", "mpgpu_plan_seed_shared"):
         getattr(L, fn).argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
         getattr(L, fn).restype = ctypes.c_int
+    L.mpgpu_plan_coarse_key_ptrs.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p),
+                                             ctypes.POINTER(ctypes.c_void_p)]
+    L.mpgpu_plan_coarse_key_ptrs.restype = ctypes.c_int
+    L.mpgpu_plan_attach_coarse_keys.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    L.mpgpu_plan_attach_coarse_keys.restype = ctypes.c_int
+    L.mpgpu_plan_coarse_run.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
+    L.mpgpu_plan_coarse_run.restype = ctypes.c_int
     L.mpgpu_plan_reset_keys.argtypes = [ctypes.c_void_p]
     L.mpgpu_plan_reset_keys.restype = ctypes.c_int
     L.mpgpu_ipc_export.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int32]
@@ -530,6 +537,21 @@ class Plan:
         """Phase 2 (after the coarse keys are MIN-merged): this shard's warm-start
         cells, RED.MIN'd into the (shared) keys."""
         _check(lib().mpgpu_plan_seed_shared(self._p, int(shard), int(n_shards)))
+
+    def coarse_key_ptrs(self):
+        """(row_ptr, col_ptr) of the nested coarse plan's own keys, or (None, None)
+        without a coarse phase; marks the coarse keys as shared (see coarse_run)."""
+        pr, pc = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib().mpgpu_plan_coarse_key_ptrs(self._p, ctypes.byref(pr), ctypes.byref(pc)))
+        return pr.value, pc.value
+
+    def attach_coarse_key_ptrs(self, row_ptr: int, col_ptr: int) -> None:
+        _check(lib().mpgpu_plan_attach_coarse_keys(self._p, ctypes.c_void_p(row_ptr or None),
+                                                   ctypes.c_void_p(col_ptr or None)))
+
+    def coarse_run(self, shard: int, n_shards: int) -> None:
+        """This shard of the coarse join into shared coarse keys."""
+        _check(lib().mpgpu_plan_coarse_run(self._p, int(shard), int(n_shards)))
 
     def reset_keys(self) -> None:
         """Empty the plan's own keys (the owner, before a shared-key join)."""

@@ -122,6 +122,7 @@ struct mpgpu_plan {
   // coarse warm start (K2b): a nested plan on the PAA-downsampled series
   int coarse_f = 0;  // 0: off
   bool coarse_pending = false;  // coarse join done, exploit not yet run
+  bool coarse_keys_shared = false;  // coarse keys shared across ranks: coarse_run is separate
   mpgpu_plan* coarse = nullptr;
   double* xc_a = nullptr;
   double* xc_b = nullptr;
@@ -296,24 +297,32 @@ int coarse_factor(const mpgpu_plan* p) {
   return (int)f;
 }
 
-// K2b, phase 1: PAA series and (this shard of) the coarse join.
-mpgpu_status coarse_begin(mpgpu_plan* p, int shard, int n_shards) {
+// The nested coarse plan (PAA series, window m/f), created on first use.
+mpgpu_status ensure_coarse(mpgpu_plan* p) {
+  if (p->coarse) return MPGPU_OK;
   const int f = p->coarse_f;
   const long long mc = p->m / f;
   const long long nA = p->A.n / f, nB = p->self ? nA : p->B.n / f;
-  if (!p->coarse) {
-    MPG_CUDA(cudaMalloc(&p->xc_a, sizeof(double) * nA));
-    if (!p->self) MPG_CUDA(cudaMalloc(&p->xc_b, sizeof(double) * nB));
-    const long long zc = p->self ? (p->zone + f - 1) / f : 0;
-    p->coarse = mpgpu_plan_create(p->xc_a, nA, p->self ? nullptr : p->xc_b, nB, mc, zc,
-                                  p->device, p->stream);
-    if (!p->coarse) return MPGPU_ECUDA;
-  }
+  MPG_CUDA(cudaMalloc(&p->xc_a, sizeof(double) * nA));
+  if (!p->self) MPG_CUDA(cudaMalloc(&p->xc_b, sizeof(double) * nB));
+  const long long zc = p->self ? (p->zone + f - 1) / f : 0;
+  p->coarse = mpgpu_plan_create(p->xc_a, nA, p->self ? nullptr : p->xc_b, nB, mc, zc,
+                                p->device, p->stream);
+  return p->coarse ? MPGPU_OK : MPGPU_ECUDA;
+}
+
+// K2b, phase 1: PAA series, the coarse plan's prepare and (this shard of) the
+// coarse join; with coarse keys shared across ranks the join is a separate
+// step (mpgpu_plan_coarse_run) once the owner's coarse prepare is visible.
+mpgpu_status coarse_begin(mpgpu_plan* p, int shard, int n_shards, bool run = true) {
+  const int f = p->coarse_f;
+  const long long nA = p->A.n / f, nB = p->self ? nA : p->B.n / f;
+  if (mpgpu_status st = ensure_coarse(p); st != MPGPU_OK) return st;
   k_paa<<<(unsigned)((nA + 255) / 256), 256, 0, p->stream>>>(p->A.x, nA, f, p->xc_a);
   if (!p->self) k_paa<<<(unsigned)((nB + 255) / 256), 256, 0, p->stream>>>(p->B.x, nB, f, p->xc_b);
   p->launches += p->self ? 1 : 2;
   mpgpu_status st = mpgpu_plan_prepare(p->coarse);
-  if (st == MPGPU_OK) st = mpgpu_plan_run(p->coarse, shard, n_shards);
+  if (st == MPGPU_OK && run) st = mpgpu_plan_run(p->coarse, shard, n_shards);
   if (st != MPGPU_OK) return st;
   p->launches += p->coarse->launches;
   MPG_CUDA(cudaGetLastError());
@@ -338,11 +347,11 @@ mpgpu_status coarse_finish(mpgpu_plan* p, int shard = 0, int n_shards = 1) {
   const long long c0 = Lc * shard / n_shards, c1 = Lc * (shard + 1) / n_shards;
   if (r1 > r0)
     k_coarse_exploit<<<(unsigned)(((r1 - r0) * nd + 255) / 256), 256, 0, p->stream>>>(
-        P.pass[0], c->key0, r0, r1, c->imask, false, f, dspan, p->zone, p->self, (int)p->m,
+        P.pass[0], key_row(c), r0, r1, c->imask, false, f, dspan, p->zone, p->self, (int)p->m,
         p->imask);
   if (c1 > c0)
     k_coarse_exploit<<<(unsigned)(((c1 - c0) * nd + 255) / 256), 256, 0, p->stream>>>(
-        P.pass[0], c->key1, c0, c1, c->imask, true, f, dspan, p->zone, p->self, (int)p->m,
+        P.pass[0], key_col(c), c0, c1, c->imask, true, f, dspan, p->zone, p->self, (int)p->m,
         p->imask);
   p->launches += 2;
   MPG_CUDA(cudaGetLastError());
@@ -558,14 +567,51 @@ mpgpu_status mpgpu_plan_prepare_shared(mpgpu_plan* p, int32_t shard, int32_t n_s
   if (st != MPGPU_OK) return st;
   if (!p->self && (st = launch_stats(p, p->B)) != MPGPU_OK) return st;
   if (p->coarse_f > 0) {
-    if (coarse_begin(p, shard, n_shards) == MPGPU_OK) {
+    if (coarse_begin(p, shard, n_shards, !p->coarse_keys_shared) == MPGPU_OK) {
       p->coarse_pending = true;
+    } else if (p->coarse_keys_shared) {
+      return fail(MPGPU_ECUDA, "coarse phase failed with shared coarse keys");
     } else {
       p->coarse_f = 0;
       cudaGetLastError();
     }
   }
   MPG_CUDA(cudaGetLastError());
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_plan_coarse_key_ptrs(mpgpu_plan* p, int64_t** d_row_keys, int64_t** d_col_keys) {
+  if (!p || !d_row_keys || !d_col_keys) return fail(MPGPU_EPARAM, "null argument");
+  *d_row_keys = *d_col_keys = nullptr;
+  if (p->coarse_f <= 0 || p->subset) return MPGPU_OK;
+  MPG_CUDA(cudaSetDevice(p->device));
+  if (mpgpu_status st = ensure_coarse(p); st != MPGPU_OK) return st;
+  *d_row_keys = (int64_t*)key_row(p->coarse);
+  *d_col_keys = (int64_t*)key_col(p->coarse);
+  p->coarse_keys_shared = true;
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_plan_attach_coarse_keys(mpgpu_plan* p, int64_t* d_row_keys, int64_t* d_col_keys) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (p->coarse_f <= 0) {
+    if (d_row_keys) return fail(MPGPU_EPARAM, "plan has no coarse phase");
+    return MPGPU_OK;
+  }
+  MPG_CUDA(cudaSetDevice(p->device));
+  if (mpgpu_status st = ensure_coarse(p); st != MPGPU_OK) return st;
+  if (mpgpu_status st = mpgpu_plan_attach_keys(p->coarse, d_row_keys, d_col_keys); st != MPGPU_OK)
+    return st;
+  p->coarse_keys_shared = d_row_keys != nullptr;
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_plan_coarse_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (!p->coarse_pending || !p->coarse) return MPGPU_OK;
+  MPG_CUDA(cudaSetDevice(p->device));
+  if (mpgpu_status st = mpgpu_plan_run(p->coarse, shard, n_shards); st != MPGPU_OK) return st;
+  p->launches += p->coarse->launches;
   return MPGPU_OK;
 }
 

@@ -84,7 +84,8 @@ class SharedKeys:
         if rank == root:
             try:
                 hs = []
-                for ptr in plan.key_ptrs():
+                cr, cc = plan.coarse_key_ptrs()  # the coarse warm-start keys are shared too
+                for ptr in plan.key_ptrs() + ((cr, cc) if cr else ()):
                     buf = (ctypes.c_char * 64)()
                     mp._check(mp.lib().mpgpu_ipc_export(ctypes.c_void_p(ptr), buf, plan.device))
                     hs.append(bytes(buf))
@@ -93,6 +94,10 @@ class SharedKeys:
                 handles = [hs]
             except Exception as e:  # noqa: BLE001 -- tell the other ranks before raising
                 handles = [f"export failed: {e}"]
+                try:
+                    plan.attach_coarse_key_ptrs(0, 0)  # back to a per-rank coarse phase
+                except Exception:  # noqa: BLE001
+                    pass
         dist.broadcast_object_list(handles, src=root, group=group)
         if isinstance(handles[0], str):
             raise RuntimeError(handles[0])
@@ -104,6 +109,10 @@ class SharedKeys:
                 self.opened.append(p.value)
                 ptrs.append(p.value)
             plan.attach_key_ptrs(ptrs[0], ptrs[1])
+            if len(ptrs) == 4:
+                plan.attach_coarse_key_ptrs(ptrs[2], ptrs[3])
+        self.coarse_shared = len(handles[0]) == 4
+        plan._coarse_shared = self.coarse_shared
 
     @classmethod
     def try_create(cls, plan, rank: int, world: int, group=None, root: int = 0):
@@ -131,6 +140,9 @@ class SharedKeys:
 
     def close(self) -> None:
         import paper_1904_12626_b200 as mp
+        if getattr(self, "coarse_shared", False):
+            self.plan.attach_coarse_key_ptrs(0, 0)  # every rank back to its own coarse keys
+            self.plan._coarse_shared = self.coarse_shared = False
         if self.opened:
             self.plan.attach_key_ptrs(0, 0)
             for p in self.opened:
@@ -147,11 +159,20 @@ def shared_prepare(plan, rank: int, world: int, stream, group=None, root: int = 
     a coarse phase (small joins) a barrier orders the ranks after that reset."""
     import torch.distributed as dist
     plan.prepare_shared(rank, world)
-    ck = plan.coarse_keys()
-    if ck is not None:
-        merge_keys_(ck[0], ck[1], group=group, root=None)
-    else:
+    if getattr(plan, "_coarse_shared", False):
+        # shared coarse keys: the owner's coarse prepare (reset + its warm start)
+        # lands before any rank's coarse shard, and every shard before the seeding
+        stream.synchronize()
         dist.barrier(group=group)
+        plan.coarse_run(rank, world)
+        stream.synchronize()
+        dist.barrier(group=group)
+    else:
+        ck = plan.coarse_keys()
+        if ck is not None:
+            merge_keys_(ck[0], ck[1], group=group, root=None)
+        else:
+            dist.barrier(group=group)
     plan.seed_shared(rank, world)
 
 

@@ -64,9 +64,14 @@ def main():
     merge_est = key_bytes / (NVLINK_MERGE_GBS * 1e9) * 1e3
     step1 = None
     if args.shared:
+        plan.coarse_key_ptrs()  # coarse keys shared too: prepare_shared stops before the coarse join
         for N in [int(v) for v in args.ns.split(",")]:
             plan.reset_keys()
             prep = [timed(stream, lambda: plan.prepare_shared(s, N)) for s in range(N)]
+            # the coarse shards, one after another into the one coarse key set (the
+            # first sees only its own coarse cells, later ones the others' as well)
+            plan.prepare_shared(0, N)
+            coarse = [timed(stream, lambda: plan.coarse_run(s, N)) for s in range(N)]
             seed = []
             for s in range(N):  # each shard's seeding consumes the pending coarse phase: redo it
                 plan.prepare_shared(s, N)
@@ -74,7 +79,8 @@ def main():
             joins = [timed(stream, lambda: plan.run(s, N)) for s in range(N)]
             fin = timed(stream, plan.outputs)
             print(json.dumps({"config": cfg.name, "mode": "shared keys, shards in sequence", "n_shards": N,
-                              "prepare_shared_ms": prep, "seed_shared_ms": seed, "join_ms": joins,
+                              "prepare_shared_ms": prep, "coarse_run_ms": coarse,
+                              "seed_shared_ms": seed, "join_ms": joins,
                               "finalize_ms": fin}), flush=True)
         plan.close()
         return
