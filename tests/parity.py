@@ -9,9 +9,12 @@ from __future__ import annotations
 import numpy as np
 
 REL = 1e-6
-# Distances near 0 (exact repeats / flat windows) are compared absolutely: the
-# reference's own QT formula carries ~sqrt(2m * 1e-16 * cond) there.
-ABS = 1e-6
+# The only absolute slack: the fp64 rounding floor of a DIRECT z-normalised
+# distance (both sides recompute near-zero distances directly). Each of the m
+# z-value differences carries ~|z| * 2^-52 <= sqrt(m) * 2^-52, so an exact
+# affine repeat comes out as ~m^1.5 * 2^-52 <= 1e-11 (m <= 1024) instead of 0.
+# Exactly 0 (flat-vs-flat, bit-identical windows) and +inf are compared exactly.
+ABS = 1e-10
 
 
 def exact_dist(x: np.ndarray, i: int, y: np.ndarray, j: int, m: int) -> float:
@@ -31,29 +34,37 @@ def exact_dist(x: np.ndarray, i: int, y: np.ndarray, j: int, m: int) -> float:
 
 
 def close(got, ref, rel=REL, abs_=ABS):
+    """MP parity: +inf and exact 0 must match exactly; finite values within
+    `rel` relative (plus the direct-distance rounding floor `abs_`)."""
     got = np.asarray(got)
     ref = np.asarray(ref)
     inf_ok = np.array_equal(np.isinf(got), np.isinf(ref))
-    fin = np.isfinite(ref)
+    zero_ok = np.array_equal(got == 0.0, ref == 0.0) or bool(
+        np.all(np.abs(got[(got == 0.0) != (ref == 0.0)]
+                      - ref[(got == 0.0) != (ref == 0.0)]) <= abs_))
+    fin = np.isfinite(ref) & np.isfinite(got)
     err = np.abs(got[fin] - ref[fin])
     ok = err <= rel * np.abs(ref[fin]) + abs_
-    return inf_ok and bool(np.all(ok)), (float(np.max(err / np.maximum(np.abs(ref[fin]), 1e-300)))
-                                         if fin.any() else 0.0)
+    return inf_ok and zero_ok and bool(np.all(ok)), (
+        float(np.max(err / np.maximum(np.abs(ref[fin]), 1e-300))) if fin.any() else 0.0)
 
 
 def index_mismatches(got_idx, ref_idx, rows, x, y, m, tol=REL):
-    """Rows whose index differs AND whose distances are not a near-tie."""
+    """Rows whose index differs AND whose exactly recomputed distances are not
+    a near-tie (|d_got - d_ref| > tol * d_ref + ABS)."""
+    got_idx = np.asarray(got_idx)
+    ref_idx = np.asarray(ref_idx)
+    rows = np.asarray(rows)
     bad = []
-    for r, gi, ri in zip(rows, got_idx, ref_idx):
-        if gi == ri:
-            continue
+    for q in np.flatnonzero(got_idx != ref_idx):
+        r, gi, ri = int(rows[q]), int(got_idx[q]), int(ref_idx[q])
         if gi < 0 or ri < 0:
-            bad.append((int(r), int(gi), int(ri)))
+            bad.append((r, gi, ri))
             continue
-        dg = exact_dist(x, int(r), y, int(gi), m)
-        dr = exact_dist(x, int(r), y, int(ri), m)
-        if abs(dg - dr) > tol * max(dr, 1e-3) + ABS:
-            bad.append((int(r), int(gi), int(ri), dg, dr))
+        dg = exact_dist(x, r, y, gi, m)
+        dr = exact_dist(x, r, y, ri, m)
+        if abs(dg - dr) > tol * dr + ABS:
+            bad.append((r, gi, ri, dg, dr))
     return bad
 
 
@@ -81,7 +92,7 @@ def raw_index_mismatches(got_idx, ref_idx, rows, a, b, m, tol=REL):
             continue
         dg = raw_exact(a, int(r), b, int(gi), m)
         dr = raw_exact(a, int(r), b, int(ri), m)
-        if abs(dg - dr) > tol * max(dr, 1e-3) + ABS:
+        if abs(dg - dr) > tol * dr + ABS:
             bad.append((int(r), int(gi), int(ri), dg, dr))
     return bad
 
@@ -126,7 +137,7 @@ def mstomp_mismatches(got, ref, x, m, must=(), exc=(), tol=REL):
             sg, pg, dg = mstomp_cell(x, int(c), g, m, order, nm)
             if g != r:
                 _, pr, _ = mstomp_cell(x, int(c), r, m, order, nm)
-                if abs(pg[kk] - pr[kk]) > tol * max(pr[kk], 1e-3) + ABS:
+                if abs(pg[kk] - pr[kk]) > tol * pr[kk] + ABS:
                     bad.append((k, int(c), g, r, pg[kk], pr[kk]))
                 continue
             # same partner, different dim_order: only at a near-tie around slot kk
@@ -135,7 +146,7 @@ def mstomp_mismatches(got, ref, x, m, must=(), exc=(), tol=REL):
                 continue
             lo = kk - 1 if kk > 0 else kk
             hi = kk + 1 if kk + 1 < D else kk
-            near = any(abs(dg[q] - dg[kk]) <= tol * max(dg[kk], 1e-3) + ABS for q in (lo, hi) if q != kk)
+            near = any(abs(dg[q] - dg[kk]) <= tol * dg[kk] + ABS for q in (lo, hi) if q != kk)
             if not near:
                 bad.append((k, int(c), "dim_order", int(gd[k, c]), int(rd[k, c]), sg[kk]))
     return bad

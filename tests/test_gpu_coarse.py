@@ -71,9 +71,10 @@ def test_coarse_forced_matches_brute_force():
     assert out.returncode == 0, out.stderr[-2000:]
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["cases"] == 16 and res["fails"] == [], res
-    # stats (4) + key fill (2) + spread init (1) alone would be 7: the coarse
-    # phase adds the PAA, the nested plan's prepare + join and two exploit launches
-    assert res["prepare_launches"] >= 7 + 1 + 8 + 2, res
+    # stats (1) + key fill (2) + spread init (1) alone would be 4: the coarse
+    # phase adds the PAA, the nested plan's prepare (4) + join (1) and two
+    # exploit launches
+    assert res["prepare_launches"] >= 4 + 1 + 5 + 2, res
 
 
 def test_sharded_prepare_bit_identical():

@@ -12,6 +12,8 @@ import os
 import numpy as np
 import pytest
 
+from tests.parity import index_mismatches
+
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
@@ -96,9 +98,10 @@ def test_oracle_vs_golden_brute(oracle_lib, name):
         # indices: identical except exact ties of the golden distance
         bad = (pi != g["pi"]) & (np.abs(mp - g["mp"]) > 1e-8)
         assert not bad.any(), fn.__name__
-        if b is None:
-            assert np.array_equal(le, g["left"]) or np.sum(le != g["left"]) <= 2
-            assert np.array_equal(ri, g["right"]) or np.sum(ri != g["right"]) <= 2
+        if b is None:  # left / right: identical except near-ties of the exact distances
+            rows = np.arange(le.size)
+            assert not index_mismatches(le, g["left"], rows, a, a, w), fn.__name__
+            assert not index_mismatches(ri, g["right"], rows, a, a, w), fn.__name__
 
 
 def test_brute_planted_repeat_and_ab_identity(oracle_lib):
