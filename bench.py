@@ -7,7 +7,8 @@ Step = one full self-join of the workload (window stats + diagonal tiles +
 finalize) with inputs resident in HBM. N=1 runs C4 (n=2^20, m=256, ECG-like,
 the headline metric's shape). Under torchrun (N>1) every rank evaluates an
 equal-cell shard of the diagonal work items, the packed int64 keys are
-min-reduced over NCCL (torch.distributed, ReduceOp.MIN) and rank 0 finalizes
+merged by RED.MIN into one key region striped over every GPU's HBM (or, with
+MPGPU_SHARED_KEYS=0, min-reduced over NCCL afterwards) and rank 0 finalizes
 (strong scaling: total work fixed). Rank 0 prints ONE JSON line.
 
 `--impl reference` times the CPU restatement of the reference STOMP
@@ -112,10 +113,11 @@ def cpu_model() -> str:
     return platform.processor() or "unknown"
 
 
-def cpu_sample_rate(cfg, seconds_target=15.0, threads=None):
+def cpu_sample_rate(cfg, seconds_target=15.0, threads=None, detail=False):
     """Oracle STOMP (restated reference, oracle/) on a bounded row sample.
 
-    Returns (unique-cells/s, threads, sample description). Full STOMP rows cost
+    Returns (unique-cells/s, threads, sample description[, detail dict with the
+    rows timed, the rows of the job and the measured seconds]). Full STOMP rows cost
     L evaluations each and L rows cover the (L-z-1)(L-z)/2 unique cells, so a
     sample of R rows stands for R/L of the job. A 256-row probe sizes the
     sample to about `seconds_target` seconds."""
@@ -134,8 +136,26 @@ def cpu_sample_rate(cfg, seconds_target=15.0, threads=None):
     else:
         rows = probe
     rate = cfg.cells() * (rows / Lrows) / dt
-    return rate, threads, (f"oracle STOMP (restated reference) rows [0,{rows}) of {Lrows}, full rows, "
-                           f"{dt:.1f}s on {threads} threads, extrapolated to unique cells")
+    desc = (f"oracle STOMP (restated reference) rows [0,{rows}) of {Lrows}, full rows, "
+            f"{dt:.1f}s on {threads} threads, extrapolated to unique cells")
+    if detail:
+        return rate, threads, desc, {"rows_timed": rows, "rows_total": Lrows, "seconds": dt}
+    return rate, threads, desc
+
+
+def config_dict(cfg):
+    """The `config` object of the JSON line, identical in both arms (the
+    reference arm has no tile and runs on the host, but names the same workload)."""
+    return {"workload": cfg.description, "config": cfg.name, "cells_per_step": cfg.cells(),
+            "window": cfg.window, "exclusion_zone": cfg.zone,
+            "series_checksum": checksum_of(cfg),
+            "l2": "flushed between steps (256 MB write)"}
+
+
+def checksum_of(cfg):
+    from paper_1904_12626_b200 import datasets
+    c = datasets.checksum(cfg.a)
+    return c if cfg.b is None else c + "/" + datasets.checksum(cfg.b)
 
 
 def flush_l2(buf):
@@ -146,20 +166,30 @@ def run_reference(args, cfg, rank, world):
     """--impl reference: the CPU restatement of the reference STOMP."""
     if rank != 0:
         return
-    samples = []
+    samples, secs = [], []
     threads = None
     desc = ""
+    det = {}
     for s in range(args.warmup + args.steps):
-        rate, threads, desc = cpu_sample_rate(cfg, seconds_target=args.ref_seconds)
+        rate, threads, desc, det = cpu_sample_rate(cfg, seconds_target=args.ref_seconds, detail=True)
         if s >= args.warmup:
             samples.append(rate)
+            secs.append(det["seconds"])
     v = statistics.median(samples)
+    # Each step is a bounded sample of the job (the full C4 join would take
+    # minutes on the host): ms_per_step is the measured wall time of that
+    # sample, and `extrapolated` says how the value scales it to the job.
     line = {
         "impl": "reference", "metric": "matrix-profile cells/sec", "value": v, "unit": "cells/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": cfg.cells() / v * 1e3, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": statistics.mean(secs) * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, datasets.py)",
-        "config": {"workload": cfg.description, "config": cfg.name, "cells_per_step": cfg.cells()},
+        "config": config_dict(cfg),
+        "extrapolated": {"rows_timed_per_step": det.get("rows_timed"), "rows_total": det.get("rows_total"),
+                         "cells_timed_per_step": int(cfg.cells() * det.get("rows_timed", 0)
+                                                     / max(1, det.get("rows_total", 1))),
+                         "note": "each step times STOMP rows [0, rows_timed); value = their unique-cell "
+                                 "equivalent / measured seconds (R rows of L stand for R/L of the job)"},
         "cpu_baseline": {"value": v, "unit": "cells/s", "cores": threads, "kind": "port", "sample": desc,
                          "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "cells/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -218,10 +248,11 @@ def main():
     my_cells = plan.cells(rank, world)
     l2 = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     outs = None
-    # N > 1: every rank's join RED.MINs into rank 0's keys over NVLink (CUDA IPC
-    # mappings), so the merge is fused into the compute and every shard filters
-    # against the whole job's keys; MPGPU_SHARED_KEYS=0 selects separate keys
-    # plus an NCCL MIN-reduce after the join.
+    # N > 1: the keys live in one region striped over every rank's HBM (CUDA VMM,
+    # 2 MB chunks round-robin) and mapped into every process; each rank's join
+    # RED.MINs into it over NVLink while it computes, so the merge is fused into
+    # the compute and every shard filters against the whole job's keys.
+    # MPGPU_SHARED_KEYS=0 selects separate keys plus an NCCL MIN-reduce.
     shared = None
     if world > 1 and os.environ.get("MPGPU_SHARED_KEYS", "1") != "0":
         shared = SharedKeys.try_create(plan, rank, world)
@@ -231,14 +262,14 @@ def main():
         ev[0].record(stream)
         with torch.cuda.stream(stream):
             if shared:
-                shared_prepare(plan, rank, world, stream)
+                shared_prepare(plan, rank, world)
             else:
                 sharded_prepare(plan, rank, world)  # coarse warm start sharded + MIN-merged
         ev[1].record(stream)
         plan.run(rank, world)
         ev[2].record(stream)
         if shared:
-            shared_finish(stream)
+            shared_finish(plan)
         elif world > 1:
             rk, ck = plan.keys()
             with torch.cuda.stream(stream):
@@ -311,13 +342,11 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, datasets.py)",
-            "config": {"workload": cfg.description, "config": cfg.name, "cells_per_step": cells_total,
-                       "window": cfg.window, "exclusion_zone": cfg.zone,
-                       "l2": "flushed between steps (256 MB write)",
-                       "parallelism": (f"diagonal shards x{world}, " + (
-                           "keys shared over NVLink (CUDA IPC), RED.MIN fused into the join" if shared
-                           else "NCCL MIN merge")) if world > 1 else "1 GPU",
-                       "tile": mp.lib().mpgpu_build_info().decode()},
+            "config": config_dict(cfg),
+            "parallelism": (f"diagonal shards x{world}, " + (
+                "keys striped over every GPU's HBM (CUDA VMM), RED.MIN fused into the join"
+                if shared else "NCCL MIN merge")) if world > 1 else "1 GPU",
+            "tile": mp.lib().mpgpu_build_info().decode(),
             "roofline": {"bound": "fp64", "kernel": "k_join", "kernel_note": "the fine join launch (plan.run), timed alone with CUDA events; the coarse warm-start join is a separate small k_join launch inside prepare, counted in value and ms_per_step",
                          "achieved": join_ops_per_s / 1e12, "peak": FP64_PEAK_MEASURED / 1e12,
                          "unit": "Tops/s (fp64 ops, SURVEY §8d: 6 per cell)",
@@ -389,9 +418,9 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
                 if b is not None:
                     b.copy_(pinned_b, non_blocking=True)
                 if shared:
-                    shared_prepare(plan, rank, world, stream)
+                    shared_prepare(plan, rank, world)
                     plan.run(rank, world)
-                    shared_finish(stream)
+                    shared_finish(plan)
                 else:
                     sharded_prepare(plan, rank, world)
                     plan.run(rank, world)
@@ -411,13 +440,13 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
                 times.append(float(tt[0]))
         if shared:
             shared.close()
-            dist.barrier()  # every mapping closed before the root frees its keys
+            dist.barrier()  # every mapping closed before any rank frees its chunks
         plan.close()
         t = sum(times) / len(times)
     return {"value": cfg.cells() / (t * 1e-3), "unit": "cells/s", "ms_per_step": t,
             "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h,
             "api": "mpgpu_join (C ABI)" if world == 1 else (
-                "Plan + keys shared over CUDA IPC" if shared else "Plan + torch.distributed NCCL MIN")}
+                "Plan + keys striped over the GPUs (CUDA VMM)" if shared else "Plan + torch.distributed NCCL MIN")}
 
 
 if __name__ == "__main__":

@@ -297,6 +297,64 @@ mpgpu_status mpgpu_ipc_export(const void *d_ptr, uint8_t *handle, int32_t device
 mpgpu_status mpgpu_ipc_open(const uint8_t *handle, void **d_ptr, int32_t device);
 mpgpu_status mpgpu_ipc_close(void *d_ptr, int32_t device);
 
+/* ---- striped key region (multi-GPU shared keys without a hot owner) --------
+ * Replaces the single-owner sharing above for the join's keys: one contiguous
+ * virtual range whose physical chunks (the VMM granularity, 2 MB) live in the
+ * HBM of different GPUs (chunk c on rank owners[c], by default a table that
+ * balances the modelled key reads per GPU). Every rank maps every
+ * chunk, so kernels index one flat array while the key traffic of all ranks
+ * spreads over every GPU's NVLink ports. Same protocol as the
+ * reference's worker merge (profile.hpp:66-68): element-wise min of packed
+ * keys, here done by RED.MIN.S64 during the join.
+ *
+ * One process per GPU: stripes_create (this rank's chunks), export_fd of each
+ * owned chunk (a POSIX fd; pass it to the other ranks, e.g. SCM_RIGHTS over a
+ * Unix socket), import_fd of every other chunk, then map. One process, several
+ * GPUs: stripes_create_local (maps as well). The kernels' 64-bit RED.MIN into
+ * a peer's chunk needs native peer atomics (NVLink): check mpgpu_peer_atomics
+ * for every (rank device, peer device) pair before using a region. */
+typedef struct mpgpu_stripes mpgpu_stripes;
+/* chunk size (the VMM granularity on `device`), -1 without VMM support */
+int64_t mpgpu_stripes_granularity(int32_t device);
+/* owners[c]: rank (create_local: index into devices) of chunk c; NULL -> c % n */
+mpgpu_stripes *mpgpu_stripes_create(int64_t bytes, int32_t n_ranks, int32_t rank, int32_t device,
+                                    const int32_t *owners);
+mpgpu_stripes *mpgpu_stripes_create_local(int64_t bytes, int32_t n_devices, const int32_t *devices,
+                                          const int32_t *owners);
+int64_t mpgpu_stripes_num_chunks(const mpgpu_stripes *s);
+int64_t mpgpu_stripes_chunk_bytes(const mpgpu_stripes *s);
+int32_t mpgpu_stripes_owner(const mpgpu_stripes *s, int64_t chunk);
+/* fd of an owned chunk (caller closes it after passing it on), -1 on error */
+int32_t mpgpu_stripes_export_fd(mpgpu_stripes *s, int64_t chunk);
+/* import a peer's chunk from a received fd (the caller closes the fd after) */
+mpgpu_status mpgpu_stripes_import_fd(mpgpu_stripes *s, int64_t chunk, int32_t fd);
+mpgpu_status mpgpu_stripes_map(mpgpu_stripes *s, void **d_base);
+void mpgpu_stripes_destroy(mpgpu_stripes *s);
+/* PCI bus id of a device (buf >= 16 bytes); 0 on success */
+int32_t mpgpu_device_pci_bus_id(int32_t device, char *buf, int32_t len);
+/* 1: native peer atomics from `device` to the GPU with that bus id (or the
+ * same GPU); 0: not supported; -1: that GPU is not visible to this process. */
+int32_t mpgpu_peer_atomics(int32_t device, const char *peer_pci_bus_id);
+
+/* Bytes of a shared key region for this plan (fine row + column keys, plus
+ * the coarse warm-start keys when the plan has a coarse phase). */
+int64_t mpgpu_plan_key_region_bytes(const mpgpu_plan *plan);
+/* Chunk owners balancing the modelled key reads per GPU (every 32-row tile of
+ * a work item reads 32 row and 32 column keys), largest chunk first to the
+ * least-loaded rank. Returns the chunk count (owners untouched when NULL or
+ * cap is smaller); *max_share = the busiest rank's share of all key reads. */
+int64_t mpgpu_plan_key_region_owners(const mpgpu_plan *plan, int64_t chunk_bytes, int32_t n_ranks,
+                                     int32_t *owners, int64_t cap, double *max_share);
+/* Place this plan's keys (and coarse keys) in a region of at least
+ * mpgpu_plan_key_region_bytes: every rank's plan of one join attaches the same
+ * region; exactly one (owner != 0) resets and warm-starts the keys
+ * (mpgpu_plan_reset_keys, prepare), the others read and RED.MIN only. With
+ * coarse keys in the region, prepare_shared stops before the coarse join and
+ * coarse_run runs it (as with mpgpu_plan_attach_coarse_keys).
+ * d_base == NULL detaches (back to the plan's own keys). */
+mpgpu_status mpgpu_plan_attach_key_region(mpgpu_plan *plan, void *d_base, int64_t bytes,
+                                          int32_t owner);
+
 /* Number of 256-diagonal bands of a self-join plan (0 for AB plans). */
 int64_t mpgpu_plan_num_bands(const mpgpu_plan *plan);
 

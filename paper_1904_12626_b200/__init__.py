@@ -171,6 +171,40 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_ipc_open.restype = ctypes.c_int
     L.mpgpu_ipc_close.argtypes = [ctypes.c_void_p, ctypes.c_int32]
     L.mpgpu_ipc_close.restype = ctypes.c_int
+    L.mpgpu_stripes_granularity.argtypes = [ctypes.c_int32]
+    L.mpgpu_stripes_granularity.restype = ctypes.c_int64
+    L.mpgpu_stripes_create.argtypes = [ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.POINTER(ctypes.c_int32)]
+    L.mpgpu_stripes_create.restype = ctypes.c_void_p
+    L.mpgpu_stripes_create_local.argtypes = [ctypes.c_int64, ctypes.c_int32,
+                                             ctypes.POINTER(ctypes.c_int32),
+                                             ctypes.POINTER(ctypes.c_int32)]
+    L.mpgpu_stripes_create_local.restype = ctypes.c_void_p
+    for fn in ("mpgpu_stripes_num_chunks", "mpgpu_stripes_chunk_bytes"):
+        getattr(L, fn).argtypes = [ctypes.c_void_p]
+        getattr(L, fn).restype = ctypes.c_int64
+    L.mpgpu_stripes_owner.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+    L.mpgpu_stripes_owner.restype = ctypes.c_int32
+    L.mpgpu_stripes_export_fd.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+    L.mpgpu_stripes_export_fd.restype = ctypes.c_int32
+    L.mpgpu_stripes_import_fd.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32]
+    L.mpgpu_stripes_import_fd.restype = ctypes.c_int
+    L.mpgpu_stripes_map.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+    L.mpgpu_stripes_map.restype = ctypes.c_int
+    L.mpgpu_stripes_destroy.argtypes = [ctypes.c_void_p]
+    L.mpgpu_stripes_destroy.restype = None
+    L.mpgpu_device_pci_bus_id.argtypes = [ctypes.c_int32, ctypes.c_char_p, ctypes.c_int32]
+    L.mpgpu_device_pci_bus_id.restype = ctypes.c_int32
+    L.mpgpu_peer_atomics.argtypes = [ctypes.c_int32, ctypes.c_char_p]
+    L.mpgpu_peer_atomics.restype = ctypes.c_int32
+    L.mpgpu_plan_key_region_bytes.argtypes = [ctypes.c_void_p]
+    L.mpgpu_plan_key_region_bytes.restype = ctypes.c_int64
+    L.mpgpu_plan_key_region_owners.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                                               ctypes.POINTER(ctypes.c_int32), ctypes.c_int64, _dp]
+    L.mpgpu_plan_key_region_owners.restype = ctypes.c_int64
+    L.mpgpu_plan_attach_key_region.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                               ctypes.c_int32]
+    L.mpgpu_plan_attach_key_region.restype = ctypes.c_int
     L.mpgpu_plan_num_bands.argtypes = [ctypes.c_void_p]
     L.mpgpu_plan_num_bands.restype = ctypes.c_int64
     L.mpgpu_simple_join.argtypes = [ctypes.POINTER(_SimpleArgs)]
@@ -562,6 +596,28 @@ class Plan:
         process's CUDA IPC handles); 0, 0 detaches."""
         _check(lib().mpgpu_plan_attach_keys(self._p, ctypes.c_void_p(row_ptr or None),
                                             ctypes.c_void_p(col_ptr or None)))
+
+    def key_region_bytes(self) -> int:
+        """Bytes of a shared key region for this plan (fine + coarse keys)."""
+        return int(lib().mpgpu_plan_key_region_bytes(self._p))
+
+    def attach_key_region(self, base: int, nbytes: int, owner: bool) -> None:
+        """Keep this plan's keys (and coarse keys) in a shared region, e.g. a
+        striped one (distributed.SharedKeys); base 0 detaches."""
+        _check(lib().mpgpu_plan_attach_key_region(self._p, ctypes.c_void_p(base or None),
+                                                  int(nbytes), 1 if owner else 0))
+
+    def key_region_owners(self, chunk_bytes: int, n_ranks: int):
+        """(owners, max_share): chunk owners of a striped key region balancing the
+        modelled key reads per GPU, and the busiest rank's share of them."""
+        n = int(lib().mpgpu_plan_key_region_owners(self._p, int(chunk_bytes), int(n_ranks), None, 0, None))
+        if n < 0:
+            raise ParameterError("bad chunk size or rank count")
+        own = (ctypes.c_int32 * max(n, 1))()
+        share = ctypes.c_double()
+        lib().mpgpu_plan_key_region_owners(self._p, int(chunk_bytes), int(n_ranks), own, n,
+                                           ctypes.byref(share))
+        return list(own)[:n], share.value
 
     def key_ptrs(self):
         """(row_ptr, col_ptr): device addresses of the plan's own key arrays."""

@@ -119,6 +119,9 @@ struct mpgpu_plan {
   // this plan's k_join reads thresholds from and RED.MINs into them directly
   long long* ext_key0 = nullptr;
   long long* ext_key1 = nullptr;
+  // attached to a shared key region as its owner: this plan still resets and
+  // warm-starts the (shared) keys; the other ranks' plans only read and RED.MIN
+  bool ext_owner = false;
   // coarse warm start (K2b): a nested plan on the PAA-downsampled series
   int coarse_f = 0;  // 0: off
   bool coarse_pending = false;  // coarse join done, exploit not yet run
@@ -375,9 +378,12 @@ void launch_init(mpgpu_plan* p, int shard, int n_shards) {
     const int mine = n_init > shard ? (n_init - shard + n_shards - 1) / n_shards : 0;
     if (mine <= 0) continue;
     // rows per thread: long enough to amortise the m-term seed, short enough
-    // that the grid still fills the GPU (~4 resident threads-worth per SM slot)
+    // that the grid still fills the GPU (~4 resident threads-worth per SM slot).
+    // Sized from the whole job's n_init, never this shard's share: the seed
+    // points (and so every warm-start cell's rounding) must not depend on the
+    // shard count, or keys would differ in their last bits across world sizes.
     const long long fill = 148LL * 2048 * 4;
-    const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * mine / fill));
+    const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * n_init / fill));
     dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)mine);
     k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask, seg, nullptr,
                                               shard, n_shards, n_init);
@@ -630,11 +636,12 @@ mpgpu_status mpgpu_plan_seed_shared(mpgpu_plan* p, int32_t shard, int32_t n_shar
 
 mpgpu_status mpgpu_plan_reset_keys(mpgpu_plan* p) {
   if (!p) return fail(MPGPU_EPARAM, "null plan");
-  if (p->ext_key0) return fail(MPGPU_EPARAM, "an attached plan does not own its keys");
+  if (p->ext_key0 && !p->ext_owner)
+    return fail(MPGPU_EPARAM, "an attached plan does not own its keys");
   MPG_CUDA(cudaSetDevice(p->device));
   const long long L1 = p->self ? p->A.L : p->B.L;
-  k_fill_keys<<<(unsigned)((p->A.L + 255) / 256), 256, 0, p->stream>>>(p->key0, p->A.L);
-  k_fill_keys<<<(unsigned)((L1 + 255) / 256), 256, 0, p->stream>>>(p->key1, L1);
+  k_fill_keys<<<(unsigned)((p->A.L + 255) / 256), 256, 0, p->stream>>>(key_row(p), p->A.L);
+  k_fill_keys<<<(unsigned)((L1 + 255) / 256), 256, 0, p->stream>>>(key_col(p), L1);
   p->launches += 2;
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
@@ -649,7 +656,7 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
   mpgpu_status st = launch_stats(p, p->A);
   if (st != MPGPU_OK) return st;
   if (!p->self && (st = launch_stats(p, p->B)) != MPGPU_OK) return st;
-  if (p->ext_key0) {
+  if (p->ext_key0 && !p->ext_owner) {
     // keys belong to the owning plan, which initialises them. With several
     // shards this plan still runs its shard of the coarse warm-start join (on
     // its own coarse keys): the caller MIN-merges the coarse keys across ranks
@@ -666,8 +673,8 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
     return MPGPU_OK;
   }
   const long long L1 = p->self ? p->A.L : p->B.L;
-  k_fill_keys<<<(unsigned)((p->A.L + 255) / 256), 256, 0, p->stream>>>(p->key0, p->A.L);
-  k_fill_keys<<<(unsigned)((L1 + 255) / 256), 256, 0, p->stream>>>(p->key1, L1);
+  k_fill_keys<<<(unsigned)((p->A.L + 255) / 256), 256, 0, p->stream>>>(key_row(p), p->A.L);
+  k_fill_keys<<<(unsigned)((L1 + 255) / 256), 256, 0, p->stream>>>(key_col(p), L1);
   p->launches += 2;
   // warm-start keys on a few spread diagonals of every pass (full runs only:
   // an anytime run must not see cells outside its bands)
@@ -784,26 +791,26 @@ mpgpu_status mpgpu_plan_finalize(mpgpu_plan* p, double* d_mp_a, int64_t* d_pi_a,
   if (p->self && p->subset) {
     const long long thr = p->A.L * 32;
     k_finalize_self_partial<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
-        p->A.view(), p->key0, p->key1, (int)p->m, p->imask, p->d_bands, (int)p->bands.size(),
+        p->A.view(), key_row(p), key_col(p), (int)p->m, p->imask, p->d_bands, (int)p->bands.size(),
         p->A.L, d_mp_a, (long long*)d_pi_a, (long long*)d_left_a, (long long*)d_right_a);
     p->launches += 1;
   } else if (p->self) {
     const long long thr = p->A.L * 32;
     k_finalize_self<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
-        p->A.view(), p->key0, p->key1, p->zone, (int)p->m, p->imask, d_mp_a,
+        p->A.view(), key_row(p), key_col(p), p->zone, (int)p->m, p->imask, d_mp_a,
         (long long*)d_pi_a, (long long*)d_left_a, (long long*)d_right_a);
     p->launches += 1;
   } else {
     if (d_mp_a || d_pi_a) {
       const long long thr = p->A.L * 32;
       k_finalize_ab<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
-          p->A.view(), p->B.view(), p->key0, (int)p->m, p->imask, d_mp_a, (long long*)d_pi_a);
+          p->A.view(), p->B.view(), key_row(p), (int)p->m, p->imask, d_mp_a, (long long*)d_pi_a);
       p->launches += 1;
     }
     if (d_mp_b || d_pi_b) {
       const long long thr = p->B.L * 32;
       k_finalize_ab<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
-          p->B.view(), p->A.view(), p->key1, (int)p->m, p->imask, d_mp_b, (long long*)d_pi_b);
+          p->B.view(), p->A.view(), key_col(p), (int)p->m, p->imask, d_mp_b, (long long*)d_pi_b);
       p->launches += 1;
     }
   }
@@ -823,6 +830,119 @@ mpgpu_status mpgpu_plan_attach_keys(mpgpu_plan* p, int64_t* d_row_keys, int64_t*
     return fail(MPGPU_EPARAM, "attach both key arrays or neither");
   p->ext_key0 = (long long*)d_row_keys;
   p->ext_key1 = (long long*)d_col_keys;
+  if (!d_row_keys) p->ext_owner = false;
+  return MPGPU_OK;
+}
+
+namespace {
+// Layout of a plan's keys in a shared key region: fine row keys, fine column
+// keys, then (with a coarse phase) the coarse row and column keys, each
+// 256-byte aligned. The same problem gives the same layout on every rank.
+struct KeyLayout { long long off[4]; long long bytes; bool coarse; };
+KeyLayout key_layout(const mpgpu_plan* p) {
+  auto up = [](long long b) { return (b + 255) / 256 * 256; };
+  KeyLayout k{};
+  const long long Lb = p->self ? p->A.L : p->B.L;
+  k.off[0] = 0;
+  k.off[1] = up(8 * p->A.L);
+  long long end = k.off[1] + up(8 * Lb);
+  k.coarse = p->coarse_f > 0 && !p->subset;
+  if (k.coarse) {
+    const long long f = p->coarse_f, mc = p->m / f;
+    const long long Lca = p->A.n / f - mc + 1, Lcb = p->self ? Lca : p->B.n / f - mc + 1;
+    k.off[2] = end;
+    k.off[3] = end + up(8 * Lca);
+    end = k.off[3] + up(8 * Lcb);
+  }
+  k.bytes = end;
+  return k;
+}
+}  // namespace
+
+int64_t mpgpu_plan_key_region_bytes(const mpgpu_plan* p) { return p ? key_layout(p).bytes : 0; }
+
+// Chunk owners of a striped key region that balance the key traffic per GPU.
+// Model: every 32-row tile of a work item reads 32 row keys and 32 column keys
+// (k_join's per-tile prefetch), so item (kb, r0, nrows) reads row keys
+// [r0, r0 + nrows) and column keys [r0 + kb, r0 + kb + nrows + kW - 1) once
+// each. Self-join rows near 0 and columns near L carry the most cells, so the
+// hot chunks sit at the two ends of the fine keys; chunks are dealt
+// largest-load-first to the least-loaded rank (LPT). The coarse keys (a join
+// of 1/f^2 of the cells) are modelled as free.
+int64_t mpgpu_plan_key_region_owners(const mpgpu_plan* p, int64_t chunk_bytes, int32_t n_ranks,
+                                     int32_t* owners, int64_t cap, double* max_share) {
+  if (!p || chunk_bytes <= 0 || n_ranks < 1) return -1;
+  const KeyLayout k = key_layout(p);
+  const long long nch = (k.bytes + chunk_bytes - 1) / chunk_bytes;
+  if (!owners || cap < nch) return nch;
+  std::vector<double> load((size_t)nch, 0.0);
+  auto add = [&](long long base, long long i0, long long i1) {  // keys [i0, i1) of one array
+    if (i1 <= i0) return;
+    long long b0 = base + 8 * i0;
+    const long long b1 = base + 8 * i1;
+    while (b0 < b1) {
+      const long long c = b0 / chunk_bytes;
+      const long long e = std::min(b1, (c + 1) * chunk_bytes);
+      load[(size_t)c] += (double)(e - b0) / 8.0;
+      b0 = e;
+    }
+  };
+  const long long Lb = p->self ? p->A.L : p->B.L;
+  for (const Item& it : p->items) {
+    // pass 0: rows A (row keys at off[0]), columns B / A (column keys at off[1]);
+    // pass 1 (AB): rows B (keys at off[1]), columns A (keys at off[0])
+    const bool p1 = it.pass == 1;
+    const long long LR = p1 ? Lb : p->A.L, LC = p1 ? p->A.L : Lb;
+    const long long offR = p1 ? k.off[1] : k.off[0], offC = p1 ? k.off[0] : k.off[1];
+    add(offR, it.r0, std::min(LR, it.r0 + it.nrows));
+    const long long c0 = it.r0 + it.kb;
+    add(offC, std::min(LC, c0), std::min(LC, c0 + it.nrows + kW - 1));
+  }
+  std::vector<long long> order((size_t)nch);
+  for (long long c = 0; c < nch; ++c) order[(size_t)c] = c;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](long long a, long long b) { return load[(size_t)a] > load[(size_t)b]; });
+  std::vector<double> per(n_ranks, 0.0);
+  double total = 0.0;
+  for (long long c : order) {
+    int best = 0;
+    for (int r = 1; r < n_ranks; ++r)
+      if (per[r] < per[best]) best = r;
+    owners[c] = best;
+    per[best] += load[(size_t)c];
+    total += load[(size_t)c];
+  }
+  if (max_share) *max_share = total > 0 ? *std::max_element(per.begin(), per.end()) / total : 0.0;
+  return nch;
+}
+
+mpgpu_status mpgpu_plan_attach_key_region(mpgpu_plan* p, void* d_base, int64_t bytes, int32_t owner) {
+  if (!p) return fail(MPGPU_EPARAM, "null plan");
+  MPG_CUDA(cudaSetDevice(p->device));
+  if (!d_base) {
+    p->ext_key0 = p->ext_key1 = nullptr;
+    p->ext_owner = false;
+    if (p->coarse) {
+      p->coarse->ext_key0 = p->coarse->ext_key1 = nullptr;
+      p->coarse->ext_owner = false;
+    }
+    p->coarse_keys_shared = false;
+    return MPGPU_OK;
+  }
+  const KeyLayout k = key_layout(p);
+  if (bytes < k.bytes) return fail(MPGPU_EPARAM, "key region too small for this plan");
+  char* b = static_cast<char*>(d_base);
+  p->ext_key0 = reinterpret_cast<long long*>(b + k.off[0]);
+  p->ext_key1 = reinterpret_cast<long long*>(b + k.off[1]);
+  p->ext_owner = owner != 0;
+  p->coarse_keys_shared = false;
+  if (k.coarse) {
+    if (mpgpu_status st = ensure_coarse(p); st != MPGPU_OK) return st;
+    p->coarse->ext_key0 = reinterpret_cast<long long*>(b + k.off[2]);
+    p->coarse->ext_key1 = reinterpret_cast<long long*>(b + k.off[3]);
+    p->coarse->ext_owner = owner != 0;
+    p->coarse_keys_shared = true;
+  }
   return MPGPU_OK;
 }
 
@@ -1139,6 +1259,56 @@ struct DevCtx {
 std::mutex g_ctx_mu;
 std::vector<std::unique_ptr<DevCtx>> g_ctx;
 
+// RED.MIN.S64 from `dev` into memory on `owner` must be a native peer atomic
+// (NVLink); over plain PCIe P2P it would not be atomic against the owner's and
+// the other shards' updates.
+bool peer_atomics_between(int dev, int owner) {
+  if (dev == owner) return true;
+  int can = 0, atom = 0;
+  if (cudaDeviceCanAccessPeer(&can, dev, owner) != cudaSuccess ||
+      cudaDeviceGetP2PAttribute(&atom, cudaDevP2PAttrNativeAtomicSupported, dev, owner) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return can && atom;
+}
+
+// The striped key region of multi-device joins, cached across calls (same
+// devices and size -> reused). Calls holding the device locks serialise use.
+struct JoinRegion {
+  std::mutex mu;
+  std::vector<int32_t> devs;
+  int64_t bytes = 0;
+  mpgpu_stripes* s = nullptr;
+  void* base = nullptr;
+  std::vector<int32_t> own;
+  void* get(const std::vector<int32_t>& d, const mpgpu_plan* p) {
+    std::lock_guard<std::mutex> lk(mu);
+    const int64_t b = mpgpu_plan_key_region_bytes(p);
+    const int64_t g = mpgpu_stripes_granularity(d[0]);
+    if (g <= 0) return nullptr;
+    std::vector<int32_t> o((size_t)std::max<int64_t>(1, (b + g - 1) / g));
+    mpgpu_plan_key_region_owners(p, g, (int32_t)d.size(), o.data(), (int64_t)o.size(), nullptr);
+    if (s && d == devs && b == bytes && o == own) return base;
+    if (s) mpgpu_stripes_destroy(s);
+    s = nullptr;
+    base = nullptr;
+    s = mpgpu_stripes_create_local(b, (int32_t)d.size(), d.data(), o.data());
+    if (!s) return nullptr;
+    if (mpgpu_stripes_map(s, &base) != MPGPU_OK) {
+      mpgpu_stripes_destroy(s);
+      s = nullptr;
+      return nullptr;
+    }
+    devs = d;
+    bytes = b;
+    own = o;
+    return base;
+  }
+};
+JoinRegion g_join_region;
+
 DevCtx* get_ctx(int device, int slot) {
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   for (auto& c : g_ctx)
@@ -1239,14 +1409,29 @@ mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* tota
     if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
     else if (pe != cudaSuccess) { cudaGetLastError(); fused = false; }
   }
-  int64_t *root_r = nullptr, *root_c = nullptr;
-  mpgpu_plan_attach_keys(c0->plan, nullptr, nullptr);
-  mpgpu_plan_keys(c0->plan, &root_r, nullptr, &root_c, nullptr);
-  for (int g = 1; g < ng; ++g) {
-    mpgpu_status st = fused ? mpgpu_plan_attach_keys(ctx[g]->plan, root_r, root_c)
-                            : mpgpu_plan_attach_keys(ctx[g]->plan, nullptr, nullptr);
+  // The shared keys live in a region striped over the shard devices (2 MB
+  // chunks round-robin), so the tile prefetches of every shard spread over all
+  // GPUs' links instead of converging on device 0. Device 0's plan owns them
+  // (resets and warm-starts); the others only read and RED.MIN.
+  if (fused) {
+    for (int g = 1; g < ng && fused; ++g)
+      fused = peer_atomics_between(real(ctx[g]), real(c0));
+  }
+  void* region = nullptr;
+  if (fused) {
+    std::vector<int32_t> ds(devs.begin(), devs.end());
+    region = g_join_region.get(ds, c0->plan);
+    if (!region) fused = false;  // no VMM: peer copies + k_keys_min below
+  }
+  for (int g = 0; g < ng; ++g) {
+    mpgpu_status st = fused ? mpgpu_plan_attach_key_region(ctx[g]->plan, region,
+                                                           mpgpu_plan_key_region_bytes(c0->plan),
+                                                           g == 0)
+                            : mpgpu_plan_attach_key_region(ctx[g]->plan, nullptr, 0, 0);
     if (st != MPGPU_OK) return st;
   }
+  int64_t *root_r = nullptr, *root_c = nullptr;
+  mpgpu_plan_keys(c0->plan, &root_r, nullptr, &root_c, nullptr);
   cudaEvent_t keys_ready = nullptr;
   for (int g = 0; g < ng; ++g) {
     DevCtx* c = ctx[g];

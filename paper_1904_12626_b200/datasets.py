@@ -55,11 +55,13 @@ def random_walk(n: int, seed: int) -> np.ndarray:
 
 
 def checksum(x: np.ndarray) -> str:
-    """64-bit FNV-1a over the fp64 bytes (series_checksum, bench.hpp:39-42)."""
-    h = 0xcbf29ce484222325
-    for byte in np.ascontiguousarray(x, dtype=np.float64).tobytes()[:1 << 20]:
-        h = ((h ^ byte) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
-    return f"{h:016x}-{x.size}"
+    """Workload checksum of a series (series_checksum, bench.hpp:39-42; the
+    reference declares it without a body): BLAKE2b-64 over all fp64 bytes,
+    plus the length. Both bench arms print it, so a reader can check that they
+    timed the same input."""
+    import hashlib
+    h = hashlib.blake2b(np.ascontiguousarray(x, dtype=np.float64).tobytes(), digest_size=8)
+    return f"{h.hexdigest()}-{x.size}"
 
 
 def _starts(g: np.random.Generator, n: int, count: int, length: int, sep: int) -> np.ndarray:

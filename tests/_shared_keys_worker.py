@@ -1,6 +1,8 @@
-"""torchrun worker for tests/test_gpu_shared_keys.py: every rank shares rank
-0's keys over CUDA IPC and joins its shard; rank 0 checks the profile against
-a one-process join of the same series (bit-identical) and prints OK."""
+"""torchrun worker for tests/test_gpu_shared_keys.py: the ranks share one key
+region striped over their GPUs (here all on cuda:0, so every chunk is local
+but every rank still maps the others' chunks from file descriptors) and join
+their shards into it; rank 0 checks the profile against a one-process join of
+the same series (bit-identical) and prints OK."""
 import os
 import sys
 
@@ -30,9 +32,10 @@ def main():
     with torch.cuda.stream(stream):
         plan = mp.Plan(a, b, m, zone, stream=stream)
         shared = SharedKeys(plan, rank, world)
+        assert shared.chunks >= 1 and shared.chunk_bytes >= 1 << 21, (shared.chunks, shared.chunk_bytes)
         outs = []
         for _ in range(2):  # the second step reuses the mappings and resets the keys
-            outs.append(shared_keys_join(plan, rank, world, stream))
+            outs.append(shared_keys_join(plan, rank, world))
         shared.close()
         sep = sharded_join(plan, rank, world)  # separate keys + MIN-reduce
     torch.cuda.synchronize()

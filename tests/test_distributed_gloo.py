@@ -110,20 +110,20 @@ def test_world_size_invariance_model():
 
 
 class _FakePlan:
-    """Stands in for a Plan whose keys cannot be exported (no device here):
-    the C ABI's mpgpu_ipc_export fails and SharedKeys must not leave the
-    other ranks waiting."""
+    """Stands in for a Plan on a machine without a GPU: the C ABI can neither
+    verify native peer atomics nor create the striped region, and SharedKeys
+    must not leave the other ranks waiting."""
 
     device = 0
 
     class a:  # noqa: N801 -- mirrors Plan.a.device
         device = torch.device("cpu")
 
-    def key_ptrs(self):
-        return 4096, 8192
+    def key_region_bytes(self):
+        return 1 << 22
 
     def reset_keys(self):
-        raise AssertionError("not reached: the export fails first")
+        raise AssertionError("not reached: the region is never created")
 
 
 def _fallback_worker(rank, world, port, out_q):
@@ -136,9 +136,9 @@ def _fallback_worker(rank, world, port, out_q):
     dist.destroy_process_group()
 
 
-def test_shared_keys_fall_back_together_when_export_fails():
-    """Every rank gets None (and so keeps the NCCL merge) when the root cannot
-    export its keys; nobody hangs in the handle broadcast."""
+def test_shared_keys_fall_back_together_when_region_fails():
+    """Every rank gets None (and so keeps the NCCL merge) when the striped key
+    region cannot be set up; nobody hangs in the fd exchange."""
     ctx = tmp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -150,3 +150,47 @@ def test_shared_keys_fall_back_together_when_export_fails():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert got == {0: True, 1: True}
+
+
+def _fd_worker(rank, world, port, n_chunks, out_q):
+    """Each rank 'owns' chunks c % world == rank, each an anonymous file
+    holding (rank, chunk); after the exchange every rank reads the files it
+    received and reports which chunks came from whom."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = {}
+    for c in range(rank, n_chunks, world):
+        fd = os.memfd_create(f"chunk{c}")
+        os.write(fd, f"{rank}:{c}".encode())
+        mine[c] = fd
+    got = distributed.exchange_fds(dict(mine), rank, world)
+    seen = {}
+    for c, fd in got.items():
+        seen[c] = os.pread(fd, 64, 0).decode()
+        os.close(fd)
+    for fd in mine.values():
+        os.close(fd)
+    out_q.put((rank, seen))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n_chunks", [(2, 5), (3, 7), (2, 450)])
+def test_exchange_fds_world(world, n_chunks):
+    """The SCM_RIGHTS exchange behind the striped key region (more than one
+    message per peer at 450 chunks): every rank ends up with a working fd for
+    every chunk the other ranks own, and none of its own."""
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fd_worker, args=(r, world, port, n_chunks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        want = {c: f"{c % world}:{c}" for c in range(n_chunks) if c % world != r}
+        assert got[r] == want

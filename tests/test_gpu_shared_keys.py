@@ -1,8 +1,11 @@
-"""Multi-process join with keys shared over CUDA IPC (bench.py's N > 1 path):
-two and three ranks, all on cuda:0 (functional only; a real run has one GPU
-per rank and the mappings go over NVLink). The profile must be bit-identical
-to a one-process join: cells never change arithmetic with sharding, and the
-shared keys are the exact MIN of every rank's candidates."""
+"""Multi-process join with the keys in one region striped over the ranks'
+GPUs (bench.py's N > 1 path): two and three ranks, all on cuda:0 (functional
+only; a real run has one GPU per rank and the chunk mappings go over NVLink).
+The profile must be bit-identical to a one-process join: cells never change
+arithmetic with sharding, and the shared keys are the exact MIN of every
+rank's candidates. n = 2^19 makes the warm start's rows per thread > 1 on one
+rank, where an earlier build sized them from the shard's share (the seed
+points then moved with the world size)."""
 import os
 import socket
 import subprocess
@@ -21,7 +24,8 @@ def _free_port():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("nproc,n,m,kind", [(2, 1 << 16, 128, "self"), (3, 1 << 14, 64, "self"),
-                                            (2, 1 << 14, 100, "ab")])
+                                            (2, 1 << 14, 100, "ab"), (2, 1 << 19, 128, "self"),
+                                            (3, 1 << 18, 200, "ab")])
 def test_shared_keys_join_matches_single_process(nproc, n, m, kind):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),

@@ -18,6 +18,12 @@ term. efficiency_N = step_1 / (N * step_N), the figure the driver computes
 from bench.py lines at N GPUs.
 
     python tools/shard_times.py [--config C4] [--ns 1,2,4,8] > profiles/shard_times_r01.jsonl
+
+--traffic prints the peer-read model of the striped key region instead: the
+chunk owners mpgpu_plan_key_region_owners picks for each N, the busiest GPU's
+share of all key reads, and from the measured one-GPU join rate the remote
+key bytes per cell of a rank and the peer-read bandwidth the busiest GPU
+serves (against the single-owner layout, where one GPU serves them all).
 """
 import argparse
 import json
@@ -33,6 +39,33 @@ import paper_1904_12626_b200 as mp  # noqa: E402
 from paper_1904_12626_b200 import datasets  # noqa: E402
 
 NVLINK_MERGE_GBS = 450.0
+# k_join's per-tile prefetch: 32 row keys + 32 column keys (8 B each) per
+# 32 row-steps x 256 diagonals = 8192 cells
+KEY_BYTES_PER_CELL = 64 * 8 / 8192.0
+
+
+def traffic(plan, cfg, stream, ns):
+    import paper_1904_12626_b200 as mp
+    gran = int(mp.lib().mpgpu_stripes_granularity(plan.device))
+    plan.prepare()
+    torch.cuda.synchronize()
+    join_ms = timed(stream, lambda: plan.run(0, 1))
+    rate = cfg.cells() / (join_ms * 1e-3)  # cells/s of one GPU
+    read_gbs = rate * KEY_BYTES_PER_CELL / 1e9
+    for N in ns:
+        owners, share = plan.key_region_owners(gran, N)
+        counts = [owners.count(r) for r in range(N)]
+        print(json.dumps({
+            "config": cfg.name, "n_ranks": N, "region_bytes": plan.key_region_bytes(),
+            "chunk_bytes": gran, "chunks": len(owners), "chunks_per_rank": counts,
+            "busiest_rank_share_of_key_reads": share,
+            "key_bytes_per_cell": KEY_BYTES_PER_CELL,
+            "remote_key_bytes_per_cell_per_rank": KEY_BYTES_PER_CELL * (N - 1) / N,
+            "one_gpu_cells_per_s": rate, "key_read_gbs_per_rank": read_gbs,
+            "busiest_gpu_peer_reads_gbs": read_gbs * (N - 1) * share,
+            "single_owner_peer_reads_gbs": read_gbs * (N - 1),
+            "note": "striped: every other rank sends `share` of its key reads to the busiest GPU; "
+                    "single owner (round 1): all of them to rank 0"}), flush=True)
 
 
 def timed(stream, fn):
@@ -51,6 +84,7 @@ def main():
     ap.add_argument("--shared", action="store_true",
                     help="shared-key phases: prepare_shared / seed_shared per shard, then the shard "
                          "joins run one after another into the same keys (no reset between them)")
+    ap.add_argument("--traffic", action="store_true", help="peer-read model of the striped key region")
     args = ap.parse_args()
     cfg = datasets.get(args.config)
     stream = torch.cuda.Stream()
@@ -60,6 +94,10 @@ def main():
         plan = mp.Plan(a, b, cfg.window, cfg.zone, stream=stream)
     # warm-up: one full single-rank step
     plan.prepare(); plan.run(0, 1); plan.outputs(); torch.cuda.synchronize()
+    if args.traffic:
+        traffic(plan, cfg, stream, [int(v) for v in args.ns.split(",")])
+        plan.close()
+        return
     key_bytes = (plan.La + plan.Lb) * 8
     merge_est = key_bytes / (NVLINK_MERGE_GBS * 1e9) * 1e3
     step1 = None
