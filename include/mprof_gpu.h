@@ -13,8 +13,11 @@
  *                                     (discovery.hpp:61-79)
  *   mpgpu_mstomp                   <- mprof::mstomp (profile.hpp:91-94)
  *   mpgpu_simple_join              <- mprof::simple_join (profile.hpp:96-100)
- *   mpgpu_rolling_stats            <- mprof::rolling_mean_std (rolling.hpp:25-29)
+ *   mpgpu_rolling_stats[_host]     <- mprof::rolling_mean_std (rolling.hpp:25-29)
  *                                     + is_flat_std (rolling.hpp:21-23)
+ *   mpgpu_mass_host                <- mprof::mass_distance_profile (distance.hpp:26-33)
+ *   mpgpu_stripes_* / key regions  <- the worker merge of stomp (profile.hpp:66-68)
+ *                                     across GPUs (one key set striped over them)
  *   mpgpu_plan_*                   <- the stomp worker-chunk contract
  *                                     (SPEC.md:267): device-resident inputs,
  *                                     sharded diagonal work and a min-merge of
@@ -109,6 +112,16 @@ int64_t mpgpu_join_cells(int64_t n_a, int64_t n_b, int64_t window, int64_t zone)
  * windows -> std 0 exactly). d_means / d_stds: device, length n - window + 1. */
 mpgpu_status mpgpu_rolling_stats(const double *d_ts, int64_t n, int64_t window, double *d_means,
                                  double *d_stds, int32_t device, void *cuda_stream);
+
+/* Host-buffer forms of the two above for the C++ API (rolling_mean_std,
+ * rolling.hpp:25-29; mass_distance_profile, distance.hpp:26-33): the library
+ * copies the series (and query) in, runs K1 / K6 on `device` and copies the
+ * results back. means / stds / out: length n - window + 1. MASS here applies
+ * no exclusion zone. */
+mpgpu_status mpgpu_rolling_stats_host(const double *ts, int64_t n, int64_t window, double *means,
+                                      double *stds, int32_t device);
+mpgpu_status mpgpu_mass_host(const double *query, int64_t window, const double *ts, int64_t n,
+                             double *out, int32_t device);
 
 /* MASS distance-profile batch (mass_distance_profile, distance.hpp:26-33):
  * n_queries z-normalised distance profiles against every window of the

@@ -616,8 +616,9 @@ mpgpu_status mpgpu_plan_coarse_run(mpgpu_plan* p, int32_t shard, int32_t n_shard
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (!p->coarse_pending || !p->coarse) return MPGPU_OK;
   MPG_CUDA(cudaSetDevice(p->device));
+  const long long before = p->coarse->launches;  // its prepare was counted by coarse_begin
   if (mpgpu_status st = mpgpu_plan_run(p->coarse, shard, n_shards); st != MPGPU_OK) return st;
-  p->launches += p->coarse->launches;
+  p->launches += p->coarse->launches - before;
   return MPGPU_OK;
 }
 
@@ -1560,6 +1561,56 @@ mpgpu_status mpgpu_join(const mpgpu_join_args* args) { return join_impl(args, nu
 
 mpgpu_status mpgpu_join_timed(const mpgpu_join_args* args, double* kernel_ms, double* total_ms) {
   return join_impl(args, kernel_ms, total_ms);
+}
+
+mpgpu_status mpgpu_rolling_stats_host(const double* ts, int64_t n, int64_t window, double* means,
+                                      double* stds, int32_t device) {
+  if (!ts || !means || !stds) return fail(MPGPU_EPARAM, "null argument");
+  if (window < 4 || window > n) return fail(MPGPU_EPARAM, "window out of range");
+  const long long L = n - window + 1;
+  DevCtx* c = get_ctx(device, 0);
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (mpgpu_status st = ensure_ctx(c); st != MPGPU_OK) return st;
+  MPG_CUDA(c->xa.ensure(sizeof(double) * n));
+  MPG_CUDA(c->out_mp_a.ensure(sizeof(double) * L));
+  MPG_CUDA(c->out_pi_a.ensure(sizeof(double) * L));
+  MPG_CUDA(cudaMemcpyAsync(c->xa.ptr, ts, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  if (mpgpu_status st = mpgpu_rolling_stats((const double*)c->xa.ptr, n, window,
+                                            (double*)c->out_mp_a.ptr, (double*)c->out_pi_a.ptr,
+                                            device, c->stream);
+      st != MPGPU_OK)
+    return st;
+  MPG_CUDA(cudaMemcpyAsync(means, c->out_mp_a.ptr, sizeof(double) * L, cudaMemcpyDeviceToHost,
+                           c->stream));
+  MPG_CUDA(cudaMemcpyAsync(stds, c->out_pi_a.ptr, sizeof(double) * L, cudaMemcpyDeviceToHost,
+                           c->stream));
+  MPG_CUDA(cudaStreamSynchronize(c->stream));
+  return MPGPU_OK;
+}
+
+mpgpu_status mpgpu_mass_host(const double* query, int64_t window, const double* ts, int64_t n,
+                             double* out, int32_t device) {
+  if (!query || !ts || !out) return fail(MPGPU_EPARAM, "null argument");
+  if (window < 4 || window > n) return fail(MPGPU_EPARAM, "window out of range");
+  const long long L = n - window + 1;
+  DevCtx* c = get_ctx(device, 0);
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (mpgpu_status st = ensure_ctx(c); st != MPGPU_OK) return st;
+  MPG_CUDA(c->xa.ensure(sizeof(double) * n));
+  MPG_CUDA(c->xb.ensure(sizeof(double) * window));
+  MPG_CUDA(c->out_mp_a.ensure(sizeof(double) * L));
+  MPG_CUDA(cudaMemcpyAsync(c->xa.ptr, ts, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+  MPG_CUDA(cudaMemcpyAsync(c->xb.ptr, query, sizeof(double) * window, cudaMemcpyHostToDevice,
+                           c->stream));
+  if (mpgpu_status st = mpgpu_distance_profiles((const double*)c->xa.ptr, n, window,
+                                                (const double*)c->xb.ptr, nullptr, 1, -1,
+                                                (double*)c->out_mp_a.ptr, device, c->stream);
+      st != MPGPU_OK)
+    return st;
+  MPG_CUDA(cudaMemcpyAsync(out, c->out_mp_a.ptr, sizeof(double) * L, cudaMemcpyDeviceToHost,
+                           c->stream));
+  MPG_CUDA(cudaStreamSynchronize(c->stream));
+  return MPGPU_OK;
 }
 
 mpgpu_status mpgpu_scrimp(const mpgpu_join_args* args, int64_t s_size, uint64_t seed,

@@ -1,12 +1,17 @@
 // C++ shim: the reference's mprof::stomp / scrimp / mstomp / simple_join
-// signatures (profile.hpp:80-100) on top of the C ABI (include/mprof_gpu.h). Status codes
-// come back as the reference's exception types (error.hpp:9-19).
+// signatures (profile.hpp:80-100) and the primitives the path uses
+// (rolling.hpp:21-29, distance.hpp:12-33, profile.hpp:66-68) on top of the C
+// ABI (include/mprof_gpu.h). Status codes come back as the reference's
+// exception types (error.hpp:9-19).
 #include <algorithm>
 #include <cmath>
+#include <stdexcept>
 #include <string>
 #include <utility>
 
+#include "mprof/distance.hpp"
 #include "mprof/profile.hpp"
+#include "mprof/rolling.hpp"
 #include "mprof_gpu.h"
 
 namespace mprof {
@@ -280,6 +285,80 @@ MatrixProfile stomp_ab_reverse(const TimeSeries &ts_a, const TimeSeries &ts_b, I
   mp.data_len = ts_b.size();
   mp.data_len_b = ts_a.size();
   return mp;
+}
+
+// ---- primitives on the path (rolling.hpp, distance.hpp, profile.hpp) --------
+
+bool is_flat_std(double sd, double mean) {
+  const double scale = std::fabs(mean) > 1.0 ? std::fabs(mean) : 1.0;
+  return sd <= 1e-10 * scale;  // the rule K1 applies on the GPU (mpgpu_kernels.cuh)
+}
+
+RollingStats rolling_mean_std(std::span<const double> ts, Index window) {
+  const Index n = static_cast<Index>(ts.size());
+  check_window(window, n, "series");
+  RollingStats r;
+  r.window = window;
+  r.means.resize(static_cast<std::size_t>(n - window + 1));
+  r.stds.resize(r.means.size());
+  const mpgpu_status st =
+      mpgpu_rolling_stats_host(ts.data(), n, window, r.means.data(), r.stds.data(), 0);
+  if (st != MPGPU_OK) raise(st);
+  return r;
+}
+
+double znorm_dist_from_qt(double qt, Index w, double mu_a, double sd_a, double mu_b,
+                          double sd_b) {
+  const bool fa = sd_a == 0.0, fb = sd_b == 0.0;  // flat windows carry sd == 0 exactly
+  if (fa && fb) return 0.0;
+  if (fa || fb) return std::sqrt(static_cast<double>(w));
+  const double wd = static_cast<double>(w);
+  const double d2 = 2.0 * wd * (1.0 - (qt - wd * mu_a * mu_b) / (wd * sd_a * sd_b));
+  return std::sqrt(std::clamp(d2, 0.0, 4.0 * wd));
+}
+
+void apply_exclusion_zone_inplace(std::span<double> distances, Index center, Index zone) {
+  const Index len = static_cast<Index>(distances.size());
+  if (center < 0 || center >= len)
+    throw ParameterError("exclusion-zone center " + std::to_string(center) +
+                         " outside the profile (length " + std::to_string(len) + ")");
+  if (zone < 0) throw ParameterError("negative exclusion zone");
+  const Index lo = std::max<Index>(0, center - zone);
+  const Index hi = zone >= len ? len - 1 : std::min<Index>(len - 1, center + zone);
+  for (Index i = lo; i <= hi; ++i) distances[static_cast<std::size_t>(i)] = kInf;
+}
+
+DistanceProfile apply_exclusion_zone(DistanceProfile dp, Index center, Index zone) {
+  apply_exclusion_zone_inplace(dp.distances, center, zone);
+  return dp;
+}
+
+void merge_min(MatrixProfile &acc, const DistanceProfile &dp, Index source_index) {
+  if (acc.values.size() != dp.distances.size() || acc.index.size() != acc.values.size())
+    throw std::logic_error("merge_min: profile lengths differ");
+  for (std::size_t i = 0; i < dp.distances.size(); ++i) {
+    if (dp.distances[i] < acc.values[i]) {  // strict improvement; ties keep the incumbent
+      acc.values[i] = dp.distances[i];
+      acc.index[i] = source_index;
+    }
+  }
+}
+
+DistanceProfile mass_distance_profile(std::span<const double> query, std::span<const double> ts,
+                                      const RollingStats &stats, double query_mean,
+                                      double query_std, Index query_index) {
+  (void)query_mean;
+  (void)query_std;
+  const Index w = static_cast<Index>(query.size()), n = static_cast<Index>(ts.size());
+  check_window(w, n, "series");
+  if (stats.window != w || stats.size() != n - w + 1)
+    throw ParameterError("rolling stats do not match the query length / series");
+  DistanceProfile dp;
+  dp.query_index = query_index;
+  dp.distances.resize(static_cast<std::size_t>(n - w + 1));
+  const mpgpu_status st = mpgpu_mass_host(query.data(), w, ts.data(), n, dp.distances.data(), 0);
+  if (st != MPGPU_OK) raise(st);
+  return dp;
 }
 
 }  // namespace mprof

@@ -136,3 +136,61 @@ def test_cpp_simple_and_mstomp(exe, tmp_path, oracle_lib):
     args[-2:] = ["1", "1"]
     r = subprocess.run(args, capture_output=True, text=True)
     assert r.returncode == 2 and "ParameterError" in r.stdout
+
+
+@pytest.fixture(scope="module")
+def prim_exe(tmp_path_factory):
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    gxx = shutil.which("g++")
+    libdir = os.path.join(ROOT, "paper_1904_12626_b200")
+    out = str(tmp_path_factory.mktemp("cpp") / "primitives_example")
+    r = subprocess.run([gxx, "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "primitives_example.cpp"), "-L" + libdir,
+                        "-lmprof_b200", "-Wl,-rpath," + libdir, "-o", out],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+@pytest.mark.parametrize("n,w,q,zone", [(5000, 64, 777, 32), (4096, 4, 0, 1), (3000, 300, 2700, 150)])
+def test_cpp_primitives_vs_oracle(prim_exe, tmp_path, oracle_lib, n, w, q, zone):
+    """rolling_mean_std (K1 on the GPU), is_flat_std, mass_distance_profile (K6),
+    apply_exclusion_zone[_inplace], znorm_dist_from_qt and merge_min called from
+    C++ through the reference signatures, against the oracle's restatements."""
+    g = np.random.default_rng(n + w)
+    x = np.cumsum(g.standard_normal(n))
+    x[1000:1400] = 3.25  # flat run: sd == 0 exactly, is_flat_std true
+    inp = tmp_path / "x.f64"
+    x.tofile(inp)
+    r = subprocess.run([prim_exe, str(inp), str(w), str(q), str(zone), str(tmp_path / "o")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    info = json.loads(r.stdout.strip().splitlines()[-1])
+    L = n - w + 1
+    rd = lambda k, t=np.float64: np.fromfile(tmp_path / f"o.{k}", dtype=t)  # noqa: E731
+    mu, sd = oracle_lib.rolling_mean_std(x, w)
+    gm, gs = rd("means"), rd("stds")
+    assert gm.size == L and info["size"] == L and info["window"] == w
+    scale = np.maximum(1.0, np.abs(mu))
+    assert np.max(np.abs(gm - mu) / scale) <= 1e-12
+    flat = sd == 0.0
+    assert np.array_equal(gs == 0.0, flat) and info["flats"] == int(flat.sum())
+    assert np.max(np.abs(gs[~flat] - sd[~flat]) / sd[~flat]) <= 1e-12
+    ref = oracle_lib.mass_distance_profile(x[q:q + w], x, -1, 0)
+    assert close(rd("mass"), ref, rel=1e-9, abs_=1e-9)[0]
+    assert rd("mass")[q] == 0.0  # exact self-match (SPEC.md:95)
+    ex = ref.copy()
+    oracle_lib.apply_exclusion_zone(ex, q, zone)
+    got_ex = rd("excl")
+    assert np.array_equal(np.isinf(got_ex), np.isinf(ex)) and info["inplace_same"]
+    assert int(np.isinf(got_ex).sum()) == min(L - 1, q + zone) - max(0, q - zone) + 1
+    # znorm_dist_from_qt on direct QT against the oracle's direct distances
+    assert close(rd("qt"), ref, rel=1e-6, abs_=1e-6)[0]
+    mv, mi = rd("merged_v"), rd("merged_i", np.int64)
+    fin = np.isfinite(got_ex)
+    assert np.array_equal(mv[fin], got_ex[fin]) and np.all(mi[fin] == q)
+    assert np.allclose(mv[~fin], rd("mass")[~fin] + 0.5) and np.all(mi[~fin] == q + 1)
+    assert info["merge_len_error"] and info["window_error"] and info["zone_50_half"] == 25
+    assert info["query_index"] == q

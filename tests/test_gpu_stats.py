@@ -1,0 +1,64 @@
+"""K1 (window statistics) through its exported entry point mpgpu_rolling_stats
+/ mp.rolling_stats (rolling_mean_std + is_flat_std, rolling.hpp:21-29) against
+the oracle's direct two-pass statistics (<= 1e-12 relative) and the SPEC.md
+known answers (tests/golden/spec_kat.json), at sizes up to the
+C5 series (n = 2^23)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def mp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1904_12626_b200 as mp
+    mp.lib()
+    return mp
+
+
+def _gpu_stats(mp, x, w):
+    import torch
+    mu, sd = mp.rolling_stats(torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda(), w)
+    return mu.cpu().numpy(), sd.cpu().numpy()
+
+
+def test_spec_known_answers(mp):
+    kat = json.load(open(os.path.join(ROOT, "tests", "golden", "spec_kat.json")))
+    cases = kat["rolling_mean_std"]
+    assert len(cases) >= 2
+    for c in cases:
+        mu, sd = _gpu_stats(mp, np.array(c["ts"], dtype=np.float64), c["w"])
+        assert np.allclose(mu, c["means"], rtol=0, atol=1e-15), (c, mu)
+        assert np.allclose(sd, c["stds"], rtol=0, atol=1e-15), (c, sd)
+
+
+@pytest.mark.parametrize("n,w", [(1024, 64), (100000, 4), (1 << 20, 256), (1 << 23, 128), (70000, 9000)])
+def test_rolling_stats_vs_oracle(mp, oracle_lib, n, w):
+    g = np.random.default_rng(n ^ w)
+    x = np.cumsum(g.standard_normal(n)) + 1e3  # offset: large means, the cancellation case
+    x[n // 3:n // 3 + 2 * w] = x[n // 3]       # a flat run (sd floored to 0)
+    x[n // 2:n // 2 + w] += 1e-13 * g.standard_normal(w)  # sub-threshold wiggle: flat as well
+    mu, sd = _gpu_stats(mp, x, w)
+    rmu, rsd = oracle_lib.rolling_mean_std(x, w, threads=8)
+    assert mu.size == n - w + 1
+    assert np.max(np.abs(mu - rmu) / np.maximum(1.0, np.abs(rmu))) <= 1e-12
+    flat = rsd == 0.0
+    assert flat.any() and np.array_equal(sd == 0.0, flat)
+    assert np.max(np.abs(sd[~flat] - rsd[~flat]) / rsd[~flat]) <= 1e-12
+
+
+def test_reversal_property(mp):
+    """rolling_mean_std over a reversed series equals the reversed stats."""
+    g = np.random.default_rng(5)
+    x = np.cumsum(g.standard_normal(50000))
+    mu, sd = _gpu_stats(mp, x, 100)
+    rmu, rsd = _gpu_stats(mp, x[::-1].copy(), 100)
+    assert np.allclose(rmu[::-1], mu, rtol=1e-12, atol=1e-12)
+    assert np.allclose(rsd[::-1], sd, rtol=1e-12, atol=0)
