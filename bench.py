@@ -274,9 +274,11 @@ def main():
             rk, ck = plan.keys()
             with torch.cuda.stream(stream):
                 merge_keys_(rk, ck, root=0)  # NCCL ReduceOp.MIN on the packed int64 keys
-        if rank == 0:
-            with torch.cuda.stream(stream):
-                outs = shared_outputs(plan, rank) if shared else plan.outputs()
+        with torch.cuda.stream(stream):
+            if shared:  # every rank decodes its rows into rank 0's output region
+                outs = shared_outputs(plan, rank, shared=shared)
+            elif rank == 0:
+                outs = plan.outputs()
         ev[3].record(stream)
 
     mk = lambda: [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -426,8 +428,9 @@ def e2e_measure(args, cfg, mp, rank, world, dev, dist):
                     plan.run(rank, world)
                     rk, ck = plan.keys()
                     merge_keys_(rk, ck, root=0)
+                o = (shared_outputs(plan, rank, shared=shared) if shared
+                     else plan.outputs() if rank == 0 else None)
                 if rank == 0:
-                    o = shared_outputs(plan, rank) if shared else plan.outputs()
                     if host_out is None:
                         host_out = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in o.items()}
                     for k, v in o.items():

@@ -263,6 +263,16 @@ mpgpu_status mpgpu_plan_finalize(mpgpu_plan *plan, double *d_mp_a, int64_t *d_pi
                                  int64_t *d_left_a, int64_t *d_right_a, double *d_mp_b,
                                  int64_t *d_pi_b);
 
+/* Decode rows [L*shard/n_shards, L*(shard+1)/n_shards) of every output (A
+ * side, and the B side of an AB-join, each by its own length) into the
+ * full-length output arrays; the rest of the arrays is untouched. With keys
+ * shared across ranks (mpgpu_plan_attach_key_region) and output arrays that
+ * every rank can write (e.g. a region owned by the root), each rank decodes
+ * its share straight into the root's profile. Anytime plans: n_shards == 1. */
+mpgpu_status mpgpu_plan_finalize_shard(mpgpu_plan *plan, int32_t shard, int32_t n_shards,
+                                       double *d_mp_a, int64_t *d_pi_a, int64_t *d_left_a,
+                                       int64_t *d_right_a, double *d_mp_b, int64_t *d_pi_b);
+
 /* Anytime mode on a self-join plan: evaluate only the given diagonal bands
  * (ids as in mpgpu_scrimp_bands); prepare() then skips the warm start and
  * finalize() searches flat-window candidates band by band. n < 0 or

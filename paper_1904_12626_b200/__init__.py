@@ -127,6 +127,9 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_plan_keys.restype = ctypes.c_int
     L.mpgpu_plan_finalize.argtypes = [ctypes.c_void_p] + [ctypes.c_void_p] * 6
     L.mpgpu_plan_finalize.restype = ctypes.c_int
+    L.mpgpu_plan_finalize_shard.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32] + \
+        [ctypes.c_void_p] * 6
+    L.mpgpu_plan_finalize_shard.restype = ctypes.c_int
     L.mpgpu_keys_min_merge.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
                                        ctypes.c_int32, ctypes.c_void_p]
     L.mpgpu_keys_min_merge.restype = ctypes.c_int
@@ -640,6 +643,13 @@ class Plan:
     def finalize(self, mp_a=None, pi_a=None, left_a=None, right_a=None, mp_b=None, pi_b=None):
         _check(lib().mpgpu_plan_finalize(self._p, *[ctypes.c_void_p(_dev_ptr(t) or None)
                                                      for t in (mp_a, pi_a, left_a, right_a, mp_b, pi_b)]))
+
+    def finalize_shard(self, shard: int, n_shards: int, mp_a=None, pi_a=None, left_a=None,
+                       right_a=None, mp_b=None, pi_b=None):
+        """Decode this shard's rows of every output (mpgpu_plan_finalize_shard)."""
+        _check(lib().mpgpu_plan_finalize_shard(self._p, int(shard), int(n_shards),
+                                               *[ctypes.c_void_p(_dev_ptr(t) or None)
+                                                 for t in (mp_a, pi_a, left_a, right_a, mp_b, pi_b)]))
 
     def outputs(self):
         """Allocate and fill the MatrixProfile arrays on the device."""

@@ -71,6 +71,7 @@ struct DevSeries {
   uint8_t* flat = nullptr;
   uint32_t* words = nullptr;
   int32_t* next = nullptr;
+  int32_t* next_agg = nullptr;  // per block of kNextBlock words (k_next_word_*)
   long long n = 0, L = 0;
   int n_words = 0;
   const double* x = nullptr;
@@ -84,7 +85,9 @@ struct DevSeries {
   void release() {
     cudaFree(mu); cudaFree(inv); cudaFree(sd); cudaFree(U); cudaFree(flat); cudaFree(words);
     cudaFree(next);
+    cudaFree(next_agg);
     mu = inv = sd = nullptr; U = nullptr; flat = nullptr; words = nullptr; next = nullptr;
+    next_agg = nullptr;
   }
 };
 
@@ -106,6 +109,11 @@ struct mpgpu_plan {
   std::vector<long long> prefix;  // prefix[i] = cells of items[0..i)
   Item* d_items = nullptr;
   int* d_counter = nullptr;
+  // which shard slices of d_items hold their item list (for slice_n shards):
+  // uploaded once, reused by every later run of the same sharding
+  std::vector<char> slice_ok;
+  std::vector<long long> slice_cnt;
+  int slice_n = 0;
   int n_ctas = 0;
   long long launches = 0;
   long long seg_rows = 0;
@@ -144,6 +152,7 @@ mpgpu_status alloc_series(DevSeries& s, const double* x, long long n, long long 
   MPG_CUDA(cudaMalloc(&s.flat, s.L));
   MPG_CUDA(cudaMalloc(&s.words, sizeof(uint32_t) * s.n_words));
   MPG_CUDA(cudaMalloc(&s.next, sizeof(int32_t) * s.n_words));
+  MPG_CUDA(cudaMalloc(&s.next_agg, sizeof(int32_t) * ((s.n_words + kNextBlock - 1) / kNextBlock)));
   return MPGPU_OK;
 }
 
@@ -155,8 +164,12 @@ mpgpu_status launch_stats(mpgpu_plan* p, DevSeries& s) {
       s.x, s.mu, s.L, (int)p->m, s.U, s.inv);
   k_flat_words<<<(unsigned)((s.n_words * 32LL + bs - 1) / bs), bs, 0, p->stream>>>(
       s.flat, s.L, s.n_words, s.words);
-  k_next_word<<<1, 1024, 0, p->stream>>>(s.words, s.n_words, s.next);
-  p->launches += 4;
+  const int nb = (s.n_words + kNextBlock - 1) / kNextBlock;
+  k_next_word_local<<<nb, kNextBlock, 0, p->stream>>>(s.words, s.n_words, s.next, s.next_agg);
+  k_next_word_aggs<<<1, 1024, 0, p->stream>>>(s.next_agg, nb);
+  k_next_word_fix<<<(unsigned)((s.n_words + 255) / 256), 256, 0, p->stream>>>(s.next, s.n_words,
+                                                                              s.next_agg);
+  p->launches += 6;
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
 }
@@ -348,17 +361,28 @@ mpgpu_status coarse_finish(mpgpu_plan* p, int shard = 0, int n_shards = 1) {
   // this shard's contiguous share of the coarse windows (all of them for one shard)
   const long long r0 = Lr * shard / n_shards, r1 = Lr * (shard + 1) / n_shards;
   const long long c0 = Lc * shard / n_shards, c1 = Lc * (shard + 1) / n_shards;
+  (void)nd;
   if (r1 > r0)
-    k_coarse_exploit<<<(unsigned)(((r1 - r0) * nd + 255) / 256), 256, 0, p->stream>>>(
-        P.pass[0], key_row(c), r0, r1, c->imask, false, f, dspan, p->zone, p->self, (int)p->m,
-        p->imask);
+    k_coarse_exploit<<<(unsigned)((r1 - r0 + kExpWarps - 1) / kExpWarps), kExpWarps * 32, 0,
+                       p->stream>>>(P.pass[0], key_row(c), r0, r1, c->imask, false, f, dspan,
+                                    p->zone, p->self, (int)p->m, p->imask);
   if (c1 > c0)
-    k_coarse_exploit<<<(unsigned)(((c1 - c0) * nd + 255) / 256), 256, 0, p->stream>>>(
-        P.pass[0], key_col(c), c0, c1, c->imask, true, f, dspan, p->zone, p->self, (int)p->m,
-        p->imask);
+    k_coarse_exploit<<<(unsigned)((c1 - c0 + kExpWarps - 1) / kExpWarps), kExpWarps * 32, 0,
+                       p->stream>>>(P.pass[0], key_col(c), c0, c1, c->imask, true, f, dspan,
+                                    p->zone, p->self, (int)p->m, p->imask);
   p->launches += 2;
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
+}
+
+// Rows per thread of the warm-start kernels: one direct m-term seed, then the
+// recurrence. Long enough that the seed costs at most ~8 FMAs per cell
+// (m / 8 rows), longer still while the grid keeps ~4 resident threads per SM
+// slot, at most kInitSeg. Depends only on the problem (L, n_init, m).
+int init_rows_per_thread(long long L, long long n_init, long long m) {
+  const long long fill = 148LL * 2048 * 4;
+  const long long by_fill = L * n_init / fill;
+  return (int)std::max<long long>(1, std::min<long long>(kInitSeg, std::max(by_fill, m / 8)));
 }
 
 // Spread-diagonal warm start (K2) of a full join: this shard's share of the
@@ -377,13 +401,10 @@ void launch_init(mpgpu_plan* p, int shard, int n_shards) {
     const int n_init = n_env >= 0 ? n_env : (p->coarse_f > 0 ? 8 : kInitDiag);
     const int mine = n_init > shard ? (n_init - shard + n_shards - 1) / n_shards : 0;
     if (mine <= 0) continue;
-    // rows per thread: long enough to amortise the m-term seed, short enough
-    // that the grid still fills the GPU (~4 resident threads-worth per SM slot).
     // Sized from the whole job's n_init, never this shard's share: the seed
     // points (and so every warm-start cell's rounding) must not depend on the
     // shard count, or keys would differ in their last bits across world sizes.
-    const long long fill = 148LL * 2048 * 4;
-    const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * n_init / fill));
+    const int seg = init_rows_per_thread(ps.R.L, n_init, p->m);
     dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)mine);
     k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask, seg, nullptr,
                                               shard, n_shards, n_init);
@@ -687,8 +708,7 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
     // cells of this run), so no row's first visit fires every warp
     const Pass& ps = P.pass[0];
     const int n_init = p->n_init_diags;
-    const long long fill = 148LL * 2048 * 4;
-    const int seg = (int)std::max<long long>(1, std::min<long long>(kInitSeg, ps.R.L * n_init / fill));
+    const int seg = init_rows_per_thread(ps.R.L, n_init, p->m);
     dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)n_init);
     k_init_keys<<<grid, 256, 0, p->stream>>>(ps, p->zone + 1, ps.C.L, (int)p->m, p->imask, seg,
                                               p->d_init_diags, 0, 1, n_init);
@@ -719,35 +739,47 @@ mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
   MPG_CUDA(cudaSetDevice(p->device));
-  std::vector<Item> mine;
-  shard_items(p, shard, n_shards, mine, nullptr);
-  if (p->subset) {
-    // keep the chosen bands' items; every 8th chosen band goes first (a probe:
-    // the rest of the run then starts from thresholds that already reflect a
-    // sample of the whole subset, so far fewer cells fire). Order never changes
-    // the result: the min-merge is exact and ties go to the smaller index.
-    std::vector<Item> probe, rest;
-    for (const Item& it : mine) {
-      const auto b = std::lower_bound(p->bands.begin(), p->bands.end(), it.kb);
-      if (b == p->bands.end() || *b != it.kb) continue;
-      ((b - p->bands.begin()) % 8 == 0 ? probe : rest).push_back(it);
-    }
-    probe.insert(probe.end(), rest.begin(), rest.end());
-    mine.swap(probe);
-  }
-  if (mine.empty()) return MPGPU_OK;
   // each shard uses its own slice of the device item buffer (shards may be
-  // in flight together on one device)
+  // in flight together on one device); a slice is uploaded on its first run
+  // and reused while the sharding and the band selection stay the same
   size_t off = 0;
   for (int s = 0; s < shard; ++s) off += (p->items.size() + n_shards - 1 - s) / n_shards;
-  MPG_CUDA(cudaMemcpyAsync(p->d_items + off, mine.data(), sizeof(Item) * mine.size(),
-                           cudaMemcpyHostToDevice, p->stream));
+  if (p->slice_n != n_shards) {
+    p->slice_ok.assign((size_t)n_shards, 0);
+    p->slice_cnt.assign((size_t)n_shards, 0);
+    p->slice_n = n_shards;
+  }
+  if (!p->slice_ok[(size_t)shard]) {
+    std::vector<Item> mine;
+    shard_items(p, shard, n_shards, mine, nullptr);
+    if (p->subset) {
+      // keep the chosen bands' items; every 8th chosen band goes first (a probe:
+      // the rest of the run then starts from thresholds that already reflect a
+      // sample of the whole subset, so far fewer cells fire). Order never changes
+      // the result: the min-merge is exact and ties go to the smaller index.
+      std::vector<Item> probe, rest;
+      for (const Item& it : mine) {
+        const auto bd = std::lower_bound(p->bands.begin(), p->bands.end(), it.kb);
+        if (bd == p->bands.end() || *bd != it.kb) continue;
+        ((bd - p->bands.begin()) % 8 == 0 ? probe : rest).push_back(it);
+      }
+      probe.insert(probe.end(), rest.begin(), rest.end());
+      mine.swap(probe);
+    }
+    if (!mine.empty())
+      MPG_CUDA(cudaMemcpyAsync(p->d_items + off, mine.data(), sizeof(Item) * mine.size(),
+                               cudaMemcpyHostToDevice, p->stream));
+    p->slice_cnt[(size_t)shard] = (long long)mine.size();
+    p->slice_ok[(size_t)shard] = 1;
+  }
+  const long long n_mine = p->slice_cnt[(size_t)shard];
+  if (n_mine == 0) return MPGPU_OK;
   MPG_CUDA(cudaMemsetAsync(p->d_counter, 0, sizeof(int), p->stream));
   JoinParams P = make_params(p);
   P.items = p->d_items + off;
-  P.n_items = (int)mine.size();
+  P.n_items = (int)n_mine;
   P.counter = p->d_counter;
-  const int grid = (int)std::min<long long>(((long long)mine.size() + kWarps - 1) / kWarps, p->n_ctas);
+  const int grid = (int)std::min<long long>((n_mine + kWarps - 1) / kWarps, p->n_ctas);
   static const bool want_stats = getenv("MPGPU_STATS") && atoi(getenv("MPGPU_STATS")) > 0;
   unsigned long long* d_stats = nullptr;
   if (want_stats) {
@@ -763,7 +795,6 @@ mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
     MPG_CUDA(cudaMemcpyAsync(h, d_stats, sizeof(h), cudaMemcpyDeviceToHost, p->stream));
     MPG_CUDA(cudaStreamSynchronize(p->stream));
     long long cells = 0;
-    for (auto& it : mine) { (void)it; }
     for (size_t q = (size_t)shard; q < p->items.size(); q += (size_t)n_shards) cells += p->item_cells[q];
     fprintf(stderr, "[mpgpu stats] cells %lld warp_row_steps %.3e slow_entries %llu (%.4f%%) row_cand %llu col_cand %llu replayed_blocks %llu (%.4f%% of blocks)\n",
             cells, cells / 256.0, h[0], 100.0 * h[0] / (cells / 256.0), h[1], h[2], h[3],
@@ -786,32 +817,48 @@ mpgpu_status mpgpu_plan_keys(mpgpu_plan* p, int64_t** d_row_keys, int64_t* row_l
 mpgpu_status mpgpu_plan_finalize(mpgpu_plan* p, double* d_mp_a, int64_t* d_pi_a,
                                  int64_t* d_left_a, int64_t* d_right_a, double* d_mp_b,
                                  int64_t* d_pi_b) {
+  return mpgpu_plan_finalize_shard(p, 0, 1, d_mp_a, d_pi_a, d_left_a, d_right_a, d_mp_b, d_pi_b);
+}
+
+mpgpu_status mpgpu_plan_finalize_shard(mpgpu_plan* p, int32_t shard, int32_t n_shards,
+                                       double* d_mp_a, int64_t* d_pi_a, int64_t* d_left_a,
+                                       int64_t* d_right_a, double* d_mp_b, int64_t* d_pi_b) {
   if (!p) return fail(MPGPU_EPARAM, "null plan");
+  if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
   MPG_CUDA(cudaSetDevice(p->device));
   const int bs = 256;
+  auto rows = [&](long long L, long long& r0, long long& r1) {
+    r0 = L * shard / n_shards;
+    r1 = L * (shard + 1) / n_shards;
+    return r1 > r0;
+  };
+  auto grid = [&](long long nrows) { return (unsigned)((nrows * kFinLanes + bs - 1) / bs); };
+  long long r0, r1;
   if (p->self && p->subset) {
+    if (n_shards != 1) return fail(MPGPU_EUNSUPPORTED, "anytime runs finalize in one piece");
     const long long thr = p->A.L * 32;
     k_finalize_self_partial<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
         p->A.view(), key_row(p), key_col(p), (int)p->m, p->imask, p->d_bands, (int)p->bands.size(),
         p->A.L, d_mp_a, (long long*)d_pi_a, (long long*)d_left_a, (long long*)d_right_a);
     p->launches += 1;
   } else if (p->self) {
-    const long long thr = p->A.L * 32;
-    k_finalize_self<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
-        p->A.view(), key_row(p), key_col(p), p->zone, (int)p->m, p->imask, d_mp_a,
-        (long long*)d_pi_a, (long long*)d_left_a, (long long*)d_right_a);
-    p->launches += 1;
-  } else {
-    if (d_mp_a || d_pi_a) {
-      const long long thr = p->A.L * 32;
-      k_finalize_ab<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
-          p->A.view(), p->B.view(), key_row(p), (int)p->m, p->imask, d_mp_a, (long long*)d_pi_a);
+    if (rows(p->A.L, r0, r1)) {
+      k_finalize_self<<<grid(r1 - r0), bs, 0, p->stream>>>(
+          p->A.view(), key_row(p), key_col(p), p->zone, (int)p->m, p->imask, r0, r1, d_mp_a,
+          (long long*)d_pi_a, (long long*)d_left_a, (long long*)d_right_a);
       p->launches += 1;
     }
-    if (d_mp_b || d_pi_b) {
-      const long long thr = p->B.L * 32;
-      k_finalize_ab<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
-          p->B.view(), p->A.view(), key_col(p), (int)p->m, p->imask, d_mp_b, (long long*)d_pi_b);
+  } else {
+    if ((d_mp_a || d_pi_a) && rows(p->A.L, r0, r1)) {
+      k_finalize_ab<<<grid(r1 - r0), bs, 0, p->stream>>>(p->A.view(), p->B.view(), key_row(p),
+                                                          (int)p->m, p->imask, r0, r1, d_mp_a,
+                                                          (long long*)d_pi_a);
+      p->launches += 1;
+    }
+    if ((d_mp_b || d_pi_b) && rows(p->B.L, r0, r1)) {
+      k_finalize_ab<<<grid(r1 - r0), bs, 0, p->stream>>>(p->B.view(), p->A.view(), key_col(p),
+                                                          (int)p->m, p->imask, r0, r1, d_mp_b,
+                                                          (long long*)d_pi_b);
       p->launches += 1;
     }
   }
@@ -950,6 +997,7 @@ mpgpu_status mpgpu_plan_attach_key_region(mpgpu_plan* p, void* d_base, int64_t b
 mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int64_t n) {
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (n < 0 || !band_ids) {  // back to the full join
+    if (p->subset) p->slice_n = 0;
     p->subset = false;
     p->bands.clear();
     return MPGPU_OK;
@@ -992,6 +1040,7 @@ mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int
   }
   p->bands.swap(kb);
   p->subset = true;
+  p->slice_n = 0;  // item order changed: re-upload on the next run
   return MPGPU_OK;
 }
 

@@ -179,32 +179,71 @@ __global__ void k_flat_words(const uint8_t* __restrict__ flat, long long L, int 
   if ((threadIdx.x & 31) == 0 && w < n_words) words[w] = b;
 }
 
-// Suffix "next non-empty word" in one block (n_words <= a few million).
-__global__ void k_next_word(const uint32_t* __restrict__ words, int n_words,
-                            int32_t* __restrict__ next) {
-  __shared__ int32_t agg[1024];
-  const int t = threadIdx.x, nt = blockDim.x;
-  const int chunk = (n_words + nt - 1) / nt;
-  const int lo = t * chunk, hi = min(n_words, lo + chunk);
-  int32_t cur = -1;
-  for (int w = hi - 1; w >= lo; --w)
-    if (words[w]) cur = w;
-  agg[t] = cur;
+// "Next non-empty word" next[w] = smallest w' >= w with words[w'] != 0 (else
+// -1), a suffix-min scan in three launches: (1) within blocks of 1024 words
+// (warp ballots + a 32-entry warp suffix), each block's first non-empty word
+// into agg; (2) one block turns agg into "first non-empty word in any later
+// block"; (3) words still -1 after (1) take that value. Replaces a one-block
+// sequential scan (63 us at n = 2^20, 8 per launch of (1) and (3)).
+constexpr int kNextBlock = 1024;
+
+__global__ void __launch_bounds__(kNextBlock) k_next_word_local(const uint32_t* __restrict__ words,
+                                                                int n_words, int32_t* __restrict__ next,
+                                                                int32_t* __restrict__ agg) {
+  __shared__ int32_t wfirst[kNextBlock / 32];
+  const int w = blockIdx.x * kNextBlock + threadIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool ne = w < n_words && words[w] != 0u;
+  const unsigned m = __ballot_sync(0xffffffffu, ne);
+  const unsigned up = m & (0xffffffffu << lane);  // non-empty lanes >= this one
+  int32_t v = up ? (w - lane) + __ffs(up) - 1 : -1;
+  if (lane == 0) wfirst[wid] = m ? w + __ffs(m) - 1 : -1;
   __syncthreads();
-  if (t == 0) {  // suffix over chunk aggregates (nt entries)
-    int32_t run = -1;
-    for (int q = nt - 1; q >= 0; --q) {
-      const int32_t a = agg[q];
-      agg[q] = run;  // exclusive: first non-empty word strictly after chunk q
-      if (a >= 0) run = a;
-    }
+  if (v < 0) {  // first non-empty word in a later warp of this block
+    for (int q = wid + 1; q < kNextBlock / 32; ++q)
+      if (wfirst[q] >= 0) { v = wfirst[q]; break; }
   }
+  if (w < n_words) next[w] = v;
+  if (threadIdx.x == 0) {
+    int32_t f = -1;
+    for (int q = 0; q < kNextBlock / 32; ++q)
+      if (wfirst[q] >= 0) { f = wfirst[q]; break; }
+    agg[blockIdx.x] = f;
+  }
+}
+
+// agg[b] <- first non-empty word in blocks > b (exclusive suffix), one block.
+__global__ void __launch_bounds__(1024) k_next_word_aggs(int32_t* __restrict__ agg, int nb) {
+  __shared__ int32_t part[1024];
+  const int t = threadIdx.x;
+  const int chunk = (nb + 1023) / 1024;
+  const int lo = t * chunk, hi = min(nb, lo + chunk);
+  int32_t f = -1;
+  for (int b = hi - 1; b >= lo; --b)
+    if (agg[b] >= 0) f = agg[b];
+  part[t] = f;  // first non-empty word of this thread's chunk
   __syncthreads();
-  int32_t run = agg[t];
-  for (int w = hi - 1; w >= lo; --w) {
-    if (words[w]) run = w;
-    next[w] = run;
+  // Hillis-Steele suffix: part[t] <- first non-empty word of chunks t.. (the
+  // earliest valid entry wins)
+  for (int d = 1; d < 1024; d <<= 1) {
+    const int32_t y = t + d < 1024 ? part[t + d] : -1;
+    __syncthreads();
+    if (part[t] < 0) part[t] = y;
+    __syncthreads();
   }
+  const int32_t after0 = t + 1 < 1024 ? part[t + 1] : -1;  // first after this chunk
+  int32_t after = after0;
+  for (int b = hi - 1; b >= lo; --b) {
+    const int32_t a = agg[b];
+    agg[b] = after;
+    if (a >= 0) after = a;
+  }
+}
+
+__global__ void k_next_word_fix(int32_t* __restrict__ next, int n_words,
+                                const int32_t* __restrict__ agg) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < n_words && next[w] < 0) next[w] = agg[w / kNextBlock];
 }
 
 __device__ __forceinline__ long long next_flat(const Series& s, long long p) {
@@ -742,50 +781,103 @@ __global__ void k_paa(const double* __restrict__ x, long long nc, int f, double*
   xc[t] = s / f;
 }
 
-__global__ void k_coarse_exploit(const Pass PS, const long long* __restrict__ ckey, long long I0,
-                                 long long I1, long long cimask, bool key_is_col, int f, int span,
-                                 long long zone, bool self, int m, long long imask) {
-  const long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const int nd = 2 * span + 1;
-  const long long I = I0 + g / nd;  // coarse windows [I0, I1): this shard's share
-  if (I >= I1) return;
+// One warp per coarse window I: the nd fine diagonals around its match share
+// one row window, so their seeds are nd sliding dot products of that window
+// against one column span. The warp stages the centred row window and the
+// span in shared memory chunk by chunk (as k_join's segment seeds) and lane
+// l accumulates diagonals l, l + 32, ... (up to kExpGroups per pass over
+// blocks of 32 kExpGroups diagonals). Then each lane walks its diagonals for
+// f rows with the join's recurrence, RED.MINing into the keys. Diagonals that
+// start above the series (j0 < 0) or lie in the exclusion zone are skipped or
+// seeded where they enter, exactly as before.
+constexpr int kExpWarps = 4;
+constexpr int kExpGroups = 4;
+constexpr int kExpChunk = 128;
+constexpr int kExpSpan = 32 * kExpGroups;  // diagonals per pass
+
+struct ExpSmem {
+  double a[kExpChunk];
+  double y[kExpChunk + kExpSpan];
+};
+
+__global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
+    const Pass PS, const long long* __restrict__ ckey, long long I0, long long I1, long long cimask,
+    bool key_is_col, int f, int span, long long zone, bool self, int m, long long imask) {
+  __shared__ ExpSmem sm[kExpWarps];
+  ExpSmem& S = sm[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const long long I = I0 + (long long)blockIdx.x * kExpWarps + (threadIdx.x >> 5);
+  if (I >= I1) return;  // whole warp
   const long long kc = ckey[I];
   if (kc == kKeyNone) return;
   const long long J = kc & cimask;
   const long long Ir = key_is_col ? J : I, Jc = key_is_col ? I : J;
-  const long long i0 = Ir * f, j0 = Jc * f + (long long)(g % nd) - span;
+  const long long i0 = Ir * f;
+  const long long jbase = Jc * f - span;  // column start of diagonal offset 0
   const Series& R = PS.R;
   const Series& C = PS.C;
-  long long q0 = j0 < 0 ? -j0 : 0;
-  if (self && j0 - i0 <= zone) return;  // the whole segment lies in the zone (or below it)
-  long long qn = f;
-  qn = min(qn, R.L - i0);
-  qn = min(qn, C.L - j0);
-  if (q0 >= qn) return;
-  const long long is = i0 + q0, js = j0 + q0;
-  const double mi = R.mu[is], mj = C.mu[js];
-  const double* xi = R.x + is;
-  const double* xj = C.x + js;
-  double acc0 = 0.0, acc1 = 0.0;
-  int t = 0;
-  for (; t + 1 < m; t += 2) {
-    acc0 = fma(xi[t] - mi, xj[t] - mj, acc0);
-    acc1 = fma(xi[t + 1] - mi, xj[t + 1] - mj, acc1);
-  }
-  if (t < m) acc0 = fma(xi[t] - mi, xj[t] - mj, acc0);
-  double cov = acc0 + acc1;
-  for (long long q = q0; q < qn; ++q) {
-    const long long i = i0 + q, j = j0 + q;
-    if (q > q0) {
-      const double2 ru = R.U[i], cu = C.U[j];
-      cov = fma(ru.x, cu.y, cov);
-      cov = fma(ru.y, cu.x, cov);
+  const int nd = 2 * span + 1;
+  if (i0 >= R.L) return;
+  const double mi = R.mu[i0];
+  for (int d0 = 0; d0 < nd; d0 += kExpSpan) {
+    // seeds of diagonals d0 .. d0 + kExpSpan - 1 at row i0 (columns jbase + d)
+    double acc[kExpGroups], asum = 0.0;
+    const int ng = min(kExpGroups, (nd - d0 + 31) / 32);  // warp-uniform
+#pragma unroll
+    for (int g = 0; g < kExpGroups; ++g) acc[g] = 0.0;
+    for (int t0 = 0; t0 < m; t0 += kExpChunk) {
+      const int tc = min(kExpChunk, m - t0);
+      for (int q = lane; q < tc; q += 32) S.a[q] = R.x[i0 + t0 + q] - mi;
+      for (int q = lane; q < tc + 32 * ng; q += 32) {
+        const long long gidx = jbase + d0 + t0 + q;
+        S.y[q] = (gidx >= 0 && gidx < C.n) ? C.x[gidx] : 0.0;
+      }
+      __syncwarp();
+      for (int t = 0; t < tc; ++t) {
+        const double at = S.a[t];
+        asum += at;
+        acc[0] = fma(at, S.y[lane + t], acc[0]);
+#pragma unroll
+        for (int g = 1; g < kExpGroups; ++g)
+          if (g < ng) acc[g] = fma(at, S.y[lane + 32 * g + t], acc[g]);
+      }
+      __syncwarp();
     }
-    const double ii = R.inv[i], ij = C.inv[j];
-    if (ii == 0.0 || ij == 0.0) continue;
-    const double c = cov * (ii * ij);
-    red_min(&PS.keyR[i], mk_key(c, j, imask));
-    red_min(&PS.keyC[j], mk_key(c, i, imask));
+#pragma unroll
+    for (int g = 0; g < kExpGroups; ++g) {
+      const int d = d0 + lane + 32 * g;
+      if (d >= nd) continue;
+      const long long j0 = jbase + d;
+      if (self && j0 - i0 <= zone) continue;  // the whole segment lies in the zone (or below it)
+      long long q0 = j0 < 0 ? -j0 : 0;
+      long long qn = f;
+      qn = min(qn, R.L - i0);
+      qn = min(qn, C.L - j0);
+      if (q0 >= qn) continue;
+      double cov;
+      if (q0 == 0) {
+        cov = fma(-C.mu[j0], asum, acc[g]);
+      } else {  // enters below the first row: direct seed where it starts
+        const long long is = i0 + q0, js = j0 + q0;
+        const double mis = R.mu[is], mjs = C.mu[js];
+        double c0 = 0.0;
+        for (int t = 0; t < m; ++t) c0 = fma(R.x[is + t] - mis, C.x[js + t] - mjs, c0);
+        cov = c0;
+      }
+      for (long long q = q0; q < qn; ++q) {
+        const long long i = i0 + q, j = j0 + q;
+        if (q > q0) {
+          const double2 ru = R.U[i], cu = C.U[j];
+          cov = fma(ru.x, cu.y, cov);
+          cov = fma(ru.y, cu.x, cov);
+        }
+        const double ii = R.inv[i], ij = C.inv[j];
+        if (ii == 0.0 || ij == 0.0) continue;
+        const double c = cov * (ii * ij);
+        red_min(&PS.keyR[i], mk_key(c, j, imask));
+        red_min(&PS.keyC[j], mk_key(c, i, imask));
+      }
+    }
   }
 }
 
@@ -1181,23 +1273,72 @@ __device__ __forceinline__ double convention_or_exact(const Series& X, long long
   return warp_exact_dist(X, i, Y, j, m, lane);
 }
 
+// Finalize kernels decode kFinG windows per warp, kFinLanes lanes each: the
+// key loads, the neighbour's statistics and its window of every group are in
+// flight together (one window per warp left each warp waiting on three
+// dependent memory round trips in turn).
+constexpr int kFinG = 4;
+constexpr int kFinLanes = 32 / kFinG;
+
+// Exact z-normalised distance of window i of X and window j of Y by a group of
+// kFinLanes lanes (sub = lane within the group): d^2 = m * sum_t ((x_t - mu_i)
+// inv_i - (y_t - mu_j) inv_j)^2. Every lane of the warp must call it (the
+// group reduction shuffles the full warp); exact == false contributes 0.
+__device__ __forceinline__ double group_exact_dist(const Series& X, long long i, const Series& Y,
+                                                   long long j, bool exact, int m, int sub) {
+  double acc = 0.0;
+  if (exact) {
+    const double mi = X.mu[i], ii = X.inv[i], mj = Y.mu[j], ij = Y.inv[j];
+    const double* xi = X.x + i;
+    const double* yj = Y.x + j;
+#pragma unroll 4
+    for (int t = sub; t < m; t += kFinLanes) {
+      // rounded products (no FMA contraction): identical windows give exactly 0
+      const double d = __dmul_rn(xi[t] - mi, ii) - __dmul_rn(yj[t] - mj, ij);
+      acc = fma(d, d, acc);
+    }
+  }
+#pragma unroll
+  for (int o = kFinLanes / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  double d2 = (double)m * acc;
+  const double cap = 4.0 * (double)m;
+  d2 = d2 > cap ? cap : d2;
+  return sqrt(d2);
+}
+
+// Value at the chosen neighbour bi (-1: none): +inf, the flat-window
+// convention (distance.hpp:14-15), or the exact distance. Warp-collective.
+__device__ __forceinline__ double group_value(const Series& X, long long i, const Series& Y,
+                                              long long bi, bool valid, int m, int sub) {
+  const bool have = valid && bi >= 0;
+  const bool fi = have && X.inv[i] == 0.0, fj = have && Y.inv[bi] == 0.0;
+  const double e = group_exact_dist(X, i, Y, bi, have && !fi && !fj, m, sub);
+  if (!have) return INFINITY;
+  if (fi && fj) return 0.0;
+  if (fi || fj) return sqrt((double)m);
+  return e;
+}
+
 // Self-join: window i has right key (row keys) and left key (column keys).
 __global__ void k_finalize_self(const Series A, const long long* __restrict__ key_right,
                                 const long long* __restrict__ key_left, long long zone, int m,
-                                long long imask, double* __restrict__ mp, long long* __restrict__ pi,
+                                long long imask, long long row0, long long row1,
+                                double* __restrict__ mp, long long* __restrict__ pi,
                                 long long* __restrict__ left, long long* __restrict__ right) {
-  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (i >= A.L) return;
+  const long long gi = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / kFinLanes;
+  const int sub = threadIdx.x % kFinLanes;
+  const long long i = row0 + gi;
+  const bool valid = i < row1;
   const long long L = A.L;
-  long long rk = key_right[i], lk = key_left[i];
+  const long long ic = valid ? i : row0;  // out-of-range groups mirror a valid window
+  long long rk = key_right[ic], lk = key_left[ic];
   const double half = 0.5;
-  const long long rlo = i + zone + 1;  // smallest admissible right neighbour
-  const long long lhi = i - zone - 1;  // largest admissible left neighbour
+  const long long rlo = ic + zone + 1;  // smallest admissible right neighbour
+  const long long lhi = ic - zone - 1;  // largest admissible left neighbour
   const long long nf_r = rlo < L ? next_flat(A, rlo) : -1;
   const long long f0 = next_flat(A, 0);
   const bool nf_l = f0 >= 0 && f0 <= lhi;
-  if (A.inv[i] == 0.0) {  // flat window: distances are 0 (flat) or sqrt(m)
+  if (A.inv[ic] == 0.0) {  // flat window: distances are 0 (flat) or sqrt(m)
     rk = nf_r >= 0 ? mk_key_score(0.0, nf_r, imask)
                    : (rlo < L ? mk_key_score(half, rlo, imask) : kKeyNone);
     lk = nf_l ? mk_key_score(0.0, f0, imask) : (lhi >= 0 ? mk_key_score(half, 0, imask) : kKeyNone);
@@ -1213,9 +1354,8 @@ __global__ void k_finalize_self(const Series A, const long long* __restrict__ ke
   }
   const long long best = lk <= rk ? lk : rk;
   const long long bi = best == kKeyNone ? -1 : (best & imask);
-  double v = INFINITY;
-  if (bi >= 0) v = convention_or_exact(A, i, A, bi, m, lane);
-  if (lane == 0) {
+  const double v = group_value(A, ic, A, bi, valid, m, sub);
+  if (valid && sub == 0) {
     if (mp) mp[i] = v;
     if (pi) pi[i] = bi;
     if (left) left[i] = lk == kKeyNone ? -1 : (lk & imask);
@@ -1305,23 +1445,24 @@ __global__ void k_finalize_self_partial(const Series A, const long long* __restr
 
 // AB-join side: window i of X against every window of Y.
 __global__ void k_finalize_ab(const Series X, const Series Y, const long long* __restrict__ keys,
-                              int m, long long imask, double* __restrict__ mp,
-                              long long* __restrict__ pi) {
-  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (i >= X.L) return;
-  long long k = keys[i];
+                              int m, long long imask, long long row0, long long row1,
+                              double* __restrict__ mp, long long* __restrict__ pi) {
+  const long long gi = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / kFinLanes;
+  const int sub = threadIdx.x % kFinLanes;
+  const long long i = row0 + gi;
+  const bool valid = i < row1;
+  const long long ic = valid ? i : row0;
+  long long k = keys[ic];
   const long long fy = next_flat(Y, 0);
-  if (X.inv[i] == 0.0) {
+  if (X.inv[ic] == 0.0) {
     k = fy >= 0 ? mk_key_score(0.0, fy, imask) : mk_key_score(0.5, 0, imask);
   } else if (fy >= 0) {
     const long long kf = mk_key_score(0.5, fy, imask);
     k = kf < k ? kf : k;
   }
   const long long bi = k == kKeyNone ? -1 : (k & imask);
-  double v = INFINITY;
-  if (bi >= 0) v = convention_or_exact(X, i, Y, bi, m, lane);
-  if (lane == 0) {
+  const double v = group_value(X, ic, Y, bi, valid, m, sub);
+  if (valid && sub == 0) {
     if (mp) mp[i] = v;
     if (pi) pi[i] = bi;
   }

@@ -136,57 +136,45 @@ def exchange_fds(my_fds: dict, rank: int, world: int, group=None, timeout: float
     return got
 
 
-class SharedKeys:
-    """The join's keys in one region striped over every rank's HBM.
+def _check_peer_atomics(device: int, rank: int, world: int, group) -> str:
+    """'' when this GPU has native peer atomics to every other rank's GPU, else
+    why not (collective: gathers every rank's PCI bus id)."""
+    import torch.distributed as dist
+    import paper_1904_12626_b200 as mp
+    L = mp.lib()
+    buf = ctypes.create_string_buffer(64)
+    bus = buf.value.decode() if L.mpgpu_device_pci_bus_id(device, buf, 64) == 0 else ""
+    buses = [None] * world
+    dist.all_gather_object(buses, bus, group=group)
+    assume = os.environ.get("MPGPU_ASSUME_PEER_ATOMICS", "0") == "1"
+    for r, b in enumerate(buses):
+        if r == rank:
+            continue
+        a = L.mpgpu_peer_atomics(device, b.encode()) if b else -1
+        if a == 0 or (a < 0 and not assume):
+            return f"no verified native peer atomics between this GPU and rank {r}'s ({b or '?'})"
+    return ""
 
-    Chunk c of the region (the VMM granularity, 2 MB) lives on the rank that
-    mpgpu_plan_key_region_owners picks: chunks are dealt by modelled key
-    traffic, largest first to the least-loaded rank.
-    Every rank maps all chunks into one contiguous range and attaches its plan
-    (fine and coarse warm-start keys), so every rank's k_join reads thresholds
-    from and RED.MINs into the same keys while it computes: the min-merge is
-    fused into the join, each shard filters against the whole job's
-    best-so-far (about the one-GPU replay rate), and the key traffic spreads
-    over all GPUs' NVLink ports instead of converging on one owner
-    (DESIGN.md §7). Rank `root` owns the keys' contents: it resets and
-    warm-starts them.
 
-    Requires native peer atomics between every pair of ranks' GPUs (NVLink;
-    checked here, MPGPU_ASSUME_PEER_ATOMICS=1 skips the check when a peer GPU is
-    not visible to this process). Collective use only (every rank constructs
-    it); on failure every rank raises at the same point."""
+class Region:
+    """A device region mapped at one contiguous address in every rank, whose
+    2 MB chunks live on the ranks `owners` names (mpgpu_stripes_*): chunk fds
+    go to every other rank over SCM_RIGHTS, every rank imports and maps all of
+    them. Collective; on failure every rank raises at the same point.
+    `prepared` lets the caller do work on the mapping before the final
+    agreement (e.g. attach a plan) so that its failure is agreed on too."""
 
-    def __init__(self, plan, rank: int, world: int, group=None, root: int = 0):
-        import torch.distributed as dist
+    def __init__(self, nbytes: int, owners, rank: int, world: int, device, device_index: int,
+                 group=None, why: str = "", prepared=None):
         import paper_1904_12626_b200 as mp
         L = mp.lib()
-        self.plan, self.rank, self.world, self.root, self.group = plan, rank, world, root, group
         self._s = None
-        self.attached = False
-        dev = plan.a.device
-        # 1) native peer atomics to every other rank's GPU
-        buf = ctypes.create_string_buffer(64)
-        bus = buf.value.decode() if L.mpgpu_device_pci_bus_id(plan.device, buf, 64) == 0 else ""
-        buses = [None] * world
-        dist.all_gather_object(buses, bus, group=group)
-        assume = os.environ.get("MPGPU_ASSUME_PEER_ATOMICS", "0") == "1"
-        why = ""
-        for r, b in enumerate(buses):
-            if r == rank:
-                continue
-            a = L.mpgpu_peer_atomics(plan.device, b.encode()) if b else -1
-            if a == 0 or (a < 0 and not assume):
-                why = f"no verified native peer atomics between this GPU and rank {r}'s ({b or '?'})"
-                break
-        # 2) this rank's chunks, exported as fds
-        nbytes = 0
+        self.base = 0
+        self.nbytes = int(nbytes)
         my_fds = {}
         if not why:
-            nbytes = plan.key_region_bytes()
-            gran = L.mpgpu_stripes_granularity(plan.device)
-            owners, self.max_share = plan.key_region_owners(gran, world) if gran > 0 else ([], 0.0)
             own_arr = (ctypes.c_int32 * max(1, len(owners)))(*owners)
-            s = L.mpgpu_stripes_create(nbytes, world, rank, plan.device, own_arr) if gran > 0 else None
+            s = L.mpgpu_stripes_create(self.nbytes, world, rank, device_index, own_arr)
             if not s:
                 why = "striped region: " + L.mpgpu_last_error().decode(errors="replace")
             else:
@@ -199,47 +187,137 @@ class SharedKeys:
                         why = "export: " + L.mpgpu_last_error().decode(errors="replace")
                         break
                     my_fds[c] = fd
-        if not _agree(not why, dev, group):
-            self._close_fds(my_fds)
+        if not _agree(not why, device, group):
+            _close_fds(my_fds)
             self.close()
-            raise RuntimeError(why or "striped keys unavailable on another rank")
-        # 3) exchange, import, map, attach
+            raise RuntimeError(why or "striped region unavailable on another rank")
         try:
             got = exchange_fds(my_fds, rank, world, group=group)
         finally:
-            self._close_fds(my_fds)
+            _close_fds(my_fds)
         try:
             for c, fd in sorted(got.items()):
                 mp._check(L.mpgpu_stripes_import_fd(self._s, c, fd))
             base = ctypes.c_void_p()
             mp._check(L.mpgpu_stripes_map(self._s, ctypes.byref(base)))
-            plan.attach_key_region(base.value, nbytes, owner=rank == root)
-            self.attached = True
-            if rank == root:
-                plan.reset_keys()  # the first join starts from empty keys
-            plan.stream.synchronize()
+            self.base = base.value
+            if prepared is not None:
+                prepared(self)
             why = ""
         except Exception as e:  # noqa: BLE001 -- agreed on collectively below
             why = str(e)
         finally:
-            self._close_fds(got)
-        if not _agree(not why, dev, group):
+            _close_fds(got)
+        if not _agree(not why, device, group):
             self.close()
-            raise RuntimeError(why or "striped keys unavailable on another rank")
-        dist.barrier(group=group)  # the owner's reset is visible before anyone seeds
+            raise RuntimeError(why or "striped region unavailable on another rank")
         self.chunks = int(L.mpgpu_stripes_num_chunks(self._s))
         self.chunk_bytes = int(L.mpgpu_stripes_chunk_bytes(self._s))
+
+    def close(self) -> None:
+        import paper_1904_12626_b200 as mp
+        if self._s is not None:
+            mp.lib().mpgpu_stripes_destroy(self._s)
+            self._s = None
+            self.base = 0
+
+
+def _close_fds(fds: dict) -> None:
+    for fd in fds.values():
+        try:
+            os.close(fd)
+        except OSError:
+            pass
+    fds.clear()
+
+
+def _align(n: int, a: int = 256) -> int:
+    return (n + a - 1) // a * a
+
+
+class SharedKeys:
+    """The join's keys in one region striped over every rank's HBM, and the
+    profile in a region on the root that every rank writes its rows of.
+
+    Keys: chunk c of the region (the VMM granularity, 2 MB) lives on the rank
+    that mpgpu_plan_key_region_owners picks (chunks dealt by modelled key
+    traffic, largest first to the least-loaded rank). Every rank maps all
+    chunks into one contiguous range and attaches its plan (fine and coarse
+    warm-start keys), so every rank's k_join reads thresholds from and RED.MINs
+    into the same keys while it computes: the min-merge is fused into the join,
+    each shard filters against the whole job's best-so-far (about the one-GPU
+    replay rate), and the key traffic spreads over all GPUs' NVLink ports
+    instead of converging on one owner. Rank `root` owns the
+    keys' contents: it resets and warm-starts them.
+
+    Profile: every chunk on the root; after the join each rank decodes its
+    1/world of the rows (mpgpu_plan_finalize_shard) straight into it over
+    NVLink, so the finalize is sharded too and no gather follows.
+
+    Requires native peer atomics between every pair of ranks' GPUs (NVLink;
+    checked here, MPGPU_ASSUME_PEER_ATOMICS=1 skips the check when a peer GPU is
+    not visible to this process). Collective use only (every rank constructs
+    it); on failure every rank raises at the same point."""
+
+    def __init__(self, plan, rank: int, world: int, group=None, root: int = 0):
+        import torch.distributed as dist
+        import paper_1904_12626_b200 as mp
+        L = mp.lib()
+        self.plan, self.rank, self.world, self.root, self.group = plan, rank, world, root, group
+        self.keys = self.out = None
+        self.attached = False
+        dev = plan.a.device
+        why = _check_peer_atomics(plan.device, rank, world, group)
+        nbytes, owners, self.max_share = 0, [], 0.0
+        if not why:
+            gran = int(L.mpgpu_stripes_granularity(plan.device))
+            if gran <= 0:
+                why = "no CUDA VMM: " + L.mpgpu_last_error().decode(errors="replace")
+            else:
+                nbytes = plan.key_region_bytes()
+                owners, self.max_share = plan.key_region_owners(gran, world)
+
+        def attach(region):
+            plan.attach_key_region(region.base, nbytes, owner=rank == root)
+            self.attached = True
+            if rank == root:
+                plan.reset_keys()  # the first join starts from empty keys
+            plan.stream.synchronize()
+
+        try:
+            self.keys = Region(nbytes, owners, rank, world, dev, plan.device, group, why, attach)
+            # the profile, all on the root: mp_a, pi_a, then left/right (self) or mp_b/pi_b (AB)
+            La, Lb = plan.La, plan.Lb
+            lens = [La, La, La, La] if plan.self_join else [La, La, Lb, Lb]
+            self._out_off = [0]
+            for n in lens:
+                self._out_off.append(self._out_off[-1] + _align(8 * n))
+            gran = self.keys.chunk_bytes
+            n_out = (self._out_off[-1] + gran - 1) // gran
+            self.out = Region(self._out_off[-1], [root] * n_out, rank, world, dev, plan.device, group)
+        except Exception:
+            self.close()
+            raise
+        dist.barrier(group=group)  # the owner's reset is visible before anyone seeds
+        self.chunks, self.chunk_bytes = self.keys.chunks, self.keys.chunk_bytes
         self.coarse_shared = True
         plan._coarse_shared = True
 
-    @staticmethod
-    def _close_fds(fds: dict) -> None:
-        for fd in fds.values():
-            try:
-                os.close(fd)
-            except OSError:
-                pass
-        fds.clear()
+    def output_views(self):
+        """The profile arrays in the root's output region, as CUDA tensors on this
+        rank (the root's are local memory). Valid until the next join."""
+        import torch
+        import paper_1904_12626_b200 as mp
+        dev = torch.device("cuda", self.plan.device)
+        names = (["mp_a", "pi_a", "left_a", "right_a"] if self.plan.self_join
+                 else ["mp_a", "pi_a", "mp_b", "pi_b"])
+        lens = [self.plan.La] * 4 if self.plan.self_join else [self.plan.La] * 2 + [self.plan.Lb] * 2
+        out = {}
+        for k, (name, n) in enumerate(zip(names, lens)):
+            typ = "<f8" if name.startswith("mp") else "<i8"
+            out[name] = torch.as_tensor(mp._CudaArray(self.out.base + self._out_off[k], n, typ, self),
+                                        device=dev)
+        return out
 
     @classmethod
     def try_create(cls, plan, rank: int, world: int, group=None, root: int = 0):
@@ -263,8 +341,7 @@ class SharedKeys:
         return sk
 
     def close(self) -> None:
-        """Detach the plan (back to its own keys) and release the region."""
-        import paper_1904_12626_b200 as mp
+        """Detach the plan (back to its own keys) and release the regions."""
         if self.attached:
             try:
                 self.plan.stream.synchronize()
@@ -272,9 +349,10 @@ class SharedKeys:
             finally:
                 self.attached = False
                 self.plan._coarse_shared = self.coarse_shared = False
-        if self._s is not None:
-            mp.lib().mpgpu_stripes_destroy(self._s)
-            self._s = None
+        for r in (self.out, self.keys):
+            if r is not None:
+                r.close()
+        self.out = self.keys = None
 
 
 def shared_prepare(plan, rank: int, world: int, group=None, root: int = 0) -> None:
@@ -304,9 +382,27 @@ def shared_finish(plan, group=None) -> None:
     dist.barrier(group=group)
 
 
-def shared_outputs(plan, rank: int, root: int = 0):
-    """The root decodes the shared keys, then empties them for the next join
-    (on its stream; the next shared_prepare synchronizes it before its barrier)."""
+def shared_outputs(plan, rank: int, root: int = 0, shared=None, group=None):
+    """Decode the shared keys into the profile, then let the root empty them for
+    the next join. With `shared` (a SharedKeys) every rank decodes its 1/world of
+    the rows straight into the root's output region (collective; a barrier
+    follows, then the root resets the keys); without it the root decodes alone.
+    Returns the profile arrays on the root (with `shared`: views of its output
+    region, valid until the next join), None elsewhere."""
+    if shared is not None and shared.out is not None:
+        import torch.distributed as dist
+        world = shared.world
+        o = shared.output_views()
+        if plan.self_join:
+            plan.finalize_shard(rank, world, o["mp_a"], o["pi_a"], o["left_a"], o["right_a"])
+        else:
+            plan.finalize_shard(rank, world, o["mp_a"], o["pi_a"], mp_b=o["mp_b"], pi_b=o["pi_b"])
+        plan.stream.synchronize()
+        dist.barrier(group=group)  # every rank's rows have landed and nobody reads the keys
+        if rank != root:
+            return None
+        plan.reset_keys()
+        return o
     if rank != root:
         return None
     out = plan.outputs()
@@ -314,12 +410,13 @@ def shared_outputs(plan, rank: int, root: int = 0):
     return out
 
 
-def shared_keys_join(plan, rank: int, world: int, group=None, root: int = 0):
+def shared_keys_join(plan, rank: int, world: int, group=None, root: int = 0, shared=None):
     """One join over keys shared through SharedKeys (attached beforehand):
     shared_prepare, this rank's shard of the join straight into the shared
-    keys, shared_finish, then the root decodes the keys.
+    keys, shared_finish, then the profile is decoded (every rank its rows into
+    the root's output region when `shared` is given, else the root alone).
     Returns the MatrixProfile device arrays on the root, None elsewhere."""
     shared_prepare(plan, rank, world, group=group, root=root)
     plan.run(rank, world)
     shared_finish(plan, group=group)
-    return shared_outputs(plan, rank, root=root)
+    return shared_outputs(plan, rank, root=root, shared=shared, group=group)

@@ -35,7 +35,8 @@ def main():
         assert shared.chunks >= 1 and shared.chunk_bytes >= 1 << 21, (shared.chunks, shared.chunk_bytes)
         outs = []
         for _ in range(2):  # the second step reuses the mappings and resets the keys
-            outs.append(shared_keys_join(plan, rank, world))
+            outs.append({k: v.clone() if v is not None else v for k, v in
+                         (shared_keys_join(plan, rank, world, shared=shared) or {}).items()})
         shared.close()
         sep = sharded_join(plan, rank, world)  # separate keys + MIN-reduce
     torch.cuda.synchronize()

@@ -181,8 +181,7 @@ def test_cpp_primitives_vs_oracle(prim_exe, tmp_path, oracle_lib, n, w, q, zone)
     ref = oracle_lib.mass_distance_profile(x[q:q + w], x, -1, 0)
     assert close(rd("mass"), ref, rel=1e-9, abs_=1e-9)[0]
     assert rd("mass")[q] == 0.0  # exact self-match
-    ex = ref.copy()
-    oracle_lib.apply_exclusion_zone(ex, q, zone)
+    ex = oracle_lib.apply_exclusion_zone(ref.copy(), q, zone)
     got_ex = rd("excl")
     assert np.array_equal(np.isinf(got_ex), np.isinf(ex)) and info["inplace_same"]
     assert int(np.isinf(got_ex).sum()) == min(L - 1, q + zone) - max(0, q - zone) + 1
