@@ -375,16 +375,6 @@ mpgpu_status coarse_finish(mpgpu_plan* p, int shard = 0, int n_shards = 1) {
   return MPGPU_OK;
 }
 
-// Rows per thread of the warm-start kernels: one direct m-term seed, then the
-// recurrence. Long enough that the seed costs at most ~8 FMAs per cell
-// (m / 8 rows), longer still while the grid keeps ~4 resident threads per SM
-// slot, at most kInitSeg. Depends only on the problem (L, n_init, m).
-int init_rows_per_thread(long long L, long long n_init, long long m) {
-  const long long fill = 148LL * 2048 * 4;
-  const long long by_fill = L * n_init / fill;
-  return (int)std::max<long long>(1, std::min<long long>(kInitSeg, std::max(by_fill, m / 8)));
-}
-
 // Spread-diagonal warm start (K2) of a full join: this shard's share of the
 // n_init diagonals of every pass (all of them for one shard).
 void launch_init(mpgpu_plan* p, int shard, int n_shards) {
@@ -401,13 +391,12 @@ void launch_init(mpgpu_plan* p, int shard, int n_shards) {
     const int n_init = n_env >= 0 ? n_env : (p->coarse_f > 0 ? 8 : kInitDiag);
     const int mine = n_init > shard ? (n_init - shard + n_shards - 1) / n_shards : 0;
     if (mine <= 0) continue;
-    // Sized from the whole job's n_init, never this shard's share: the seed
-    // points (and so every warm-start cell's rounding) must not depend on the
-    // shard count, or keys would differ in their last bits across world sizes.
-    const int seg = init_rows_per_thread(ps.R.L, n_init, p->m);
-    dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)mine);
-    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask, seg, nullptr,
-                                              shard, n_shards, n_init);
+    // seed points every kInitRows rows (the problem's, never the shard's)
+    dim3 grid((unsigned)((ps.R.L + (long long)kInitWarps * kInitRows - 1) /
+                         ((long long)kInitWarps * kInitRows)),
+              (unsigned)mine);
+    k_init_keys<<<grid, kInitWarps * 32, 0, p->stream>>>(ps, klo, khi, (int)p->m, p->imask, nullptr,
+                                                         shard, n_shards, n_init);
     p->launches += 1;
   }
 }
@@ -708,10 +697,11 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
     // cells of this run), so no row's first visit fires every warp
     const Pass& ps = P.pass[0];
     const int n_init = p->n_init_diags;
-    const int seg = init_rows_per_thread(ps.R.L, n_init, p->m);
-    dim3 grid((unsigned)((ps.R.L + 256LL * seg - 1) / (256LL * seg)), (unsigned)n_init);
-    k_init_keys<<<grid, 256, 0, p->stream>>>(ps, p->zone + 1, ps.C.L, (int)p->m, p->imask, seg,
-                                              p->d_init_diags, 0, 1, n_init);
+    dim3 grid((unsigned)((ps.R.L + (long long)kInitWarps * kInitRows - 1) /
+                         ((long long)kInitWarps * kInitRows)),
+              (unsigned)n_init);
+    k_init_keys<<<grid, kInitWarps * 32, 0, p->stream>>>(ps, p->zone + 1, ps.C.L, (int)p->m,
+                                                         p->imask, p->d_init_diags, 0, 1, n_init);
     p->launches += 1;
   }
   if (npass > 0 && p->coarse_f > 0) {

@@ -719,46 +719,60 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
 #endif
 constexpr int kInitDiag = MPGPU_INIT_DIAG;
 
-constexpr int kInitSeg = 32;  // max rows per thread: one direct seed, then the recurrence
+// One warp per run of kInitRows consecutive rows of one diagonal: the warp
+// computes the run's first covariance by a direct centred dot product (lanes
+// split the m terms, butterfly sum), then 32 rows at a time each lane takes
+// its row's recurrence increment df_R dg_C + dg_R df_C and an inclusive warp
+// scan turns them into the 32 covariances (the recurrence summed as a tree).
+// All loads are coalesced and no lane walks a long dependent chain. Seed
+// points sit at multiples of kInitRows: they depend on the problem only,
+// never on the shard count.
+constexpr int kInitRows = 128;
+constexpr int kInitWarps = 8;
 
-__global__ void k_init_keys(const Pass PS, long long klo, long long khi, int m, long long imask,
-                            int seg, const long long* __restrict__ diags, int b0, int bstride,
-                            int nb_total) {
-  const long long i0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * seg;
+__global__ void __launch_bounds__(kInitWarps * 32) k_init_keys(
+    const Pass PS, long long klo, long long khi, int m, long long imask,
+    const long long* __restrict__ diags, int b0, int bstride, int nb_total) {
+  const int lane = threadIdx.x & 31;
+  const long long i0 = ((long long)blockIdx.x * kInitWarps + (threadIdx.x >> 5)) * kInitRows;
   const int b = b0 + (int)blockIdx.y * bstride;  // this launch's share of the nb_total diagonals
   const Series& R = PS.R;
   const Series& C = PS.C;
   const long long span = khi - klo;
-  if (span <= 0 || i0 >= R.L) return;
+  if (span <= 0 || i0 >= R.L) return;  // whole warp
   // diagonal b: klo + b*span/nb (b = 0 is the first admissible diagonal), or
   // the b-th entry of an explicit list (anytime runs: diagonals of chosen bands)
   const long long k = diags ? diags[b] : klo + (span * b) / (long long)nb_total;
   const long long j0 = i0 + k;
   if (j0 >= C.L) return;
-  // seed cov(i0, j0) by a direct centred dot product, then walk the diagonal
-  // with the join's recurrence (the keys only have to be values of real cells)
+  const long long n = min((long long)kInitRows, min(R.L - i0, C.L - j0));
   const double mi = R.mu[i0], mj = C.mu[j0];
   const double* xi = R.x + i0;
   const double* xj = C.x + j0;
-  double acc0 = 0.0, acc1 = 0.0;
-  int t = 0;
-  for (; t + 1 < m; t += 2) {
-    acc0 = fma(xi[t] - mi, xj[t] - mj, acc0);
-    acc1 = fma(xi[t + 1] - mi, xj[t + 1] - mj, acc1);
-  }
-  if (t < m) acc0 = fma(xi[t] - mi, xj[t] - mj, acc0);
-  double cov = acc0 + acc1;
-  const long long n = min((long long)seg, min(R.L - i0, C.L - j0));
-  for (long long s = 0; s < n; ++s) {
+  double cov = 0.0;
+  for (int t = lane; t < m; t += 32) cov = fma(xi[t] - mi, xj[t] - mj, cov);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cov += __shfl_xor_sync(0xffffffffu, cov, o);
+  for (long long s0 = 0; s0 < n; s0 += 32) {
+    const long long s = s0 + lane;
     const long long i = i0 + s, j = j0 + s;
-    if (s > 0) {
+    const bool in = s < n;
+    double inc = 0.0;
+    if (in && s > 0) {
       const double2 ru = R.U[i], cu = C.U[j];
-      cov = fma(ru.x, cu.y, cov);
-      cov = fma(ru.y, cu.x, cov);
+      inc = fma(ru.x, cu.y, ru.y * cu.x);
     }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {  // inclusive scan of the increments
+      const double v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    const double c_ij = cov + inc;
+    cov = __shfl_sync(0xffffffffu, c_ij, 31);  // the next 32 rows continue from row s0 + 31
+    if (!in) continue;
     const double ii = R.inv[i], ij = C.inv[j];
     if (ii == 0.0 || ij == 0.0) continue;
-    const double c = cov * (ii * ij);
+    const double c = c_ij * (ii * ij);
     red_min(&PS.keyR[i], mk_key(c, j, imask));
     red_min(&PS.keyC[j], mk_key(c, i, imask));
   }
@@ -795,9 +809,21 @@ constexpr int kExpGroups = 4;
 constexpr int kExpChunk = 128;
 constexpr int kExpSpan = 32 * kExpGroups;  // diagonals per pass
 
+constexpr int kExpWalk = 32;  // rows staged per walk chunk
+
 struct ExpSmem {
-  double a[kExpChunk];
-  double y[kExpChunk + kExpSpan];
+  union {
+    struct {  // seeds: centred row window chunk, column span chunk
+      double a[kExpChunk];
+      double y[kExpChunk + kExpSpan];
+    } seed;
+    struct {  // walk: rows [qc, qc + kExpWalk), the columns they meet
+      double2 rU[kExpWalk];
+      double rI[kExpWalk];
+      double2 cU[kExpSpan + kExpWalk];
+      double cI[kExpSpan + kExpWalk];
+    } walk;
+  };
 };
 
 __global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
@@ -827,56 +853,95 @@ __global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
     for (int g = 0; g < kExpGroups; ++g) acc[g] = 0.0;
     for (int t0 = 0; t0 < m; t0 += kExpChunk) {
       const int tc = min(kExpChunk, m - t0);
-      for (int q = lane; q < tc; q += 32) S.a[q] = R.x[i0 + t0 + q] - mi;
+      for (int q = lane; q < tc; q += 32) S.seed.a[q] = R.x[i0 + t0 + q] - mi;
       for (int q = lane; q < tc + 32 * ng; q += 32) {
         const long long gidx = jbase + d0 + t0 + q;
-        S.y[q] = (gidx >= 0 && gidx < C.n) ? C.x[gidx] : 0.0;
+        S.seed.y[q] = (gidx >= 0 && gidx < C.n) ? C.x[gidx] : 0.0;
       }
       __syncwarp();
       for (int t = 0; t < tc; ++t) {
-        const double at = S.a[t];
+        const double at = S.seed.a[t];
         asum += at;
-        acc[0] = fma(at, S.y[lane + t], acc[0]);
+        acc[0] = fma(at, S.seed.y[lane + t], acc[0]);
 #pragma unroll
         for (int g = 1; g < kExpGroups; ++g)
-          if (g < ng) acc[g] = fma(at, S.y[lane + 32 * g + t], acc[g]);
+          if (g < ng) acc[g] = fma(at, S.seed.y[lane + 32 * g + t], acc[g]);
       }
       __syncwarp();
     }
+    // per lane and group: the diagonal's first row q0 and end qn (q0 >= qn: skip)
+    long long q0s[kExpGroups], qns[kExpGroups];
 #pragma unroll
     for (int g = 0; g < kExpGroups; ++g) {
       const int d = d0 + lane + 32 * g;
-      if (d >= nd) continue;
       const long long j0 = jbase + d;
-      if (self && j0 - i0 <= zone) continue;  // the whole segment lies in the zone (or below it)
-      long long q0 = j0 < 0 ? -j0 : 0;
-      long long qn = f;
+      long long q0 = j0 < 0 ? -j0 : 0, qn = f;
       qn = min(qn, R.L - i0);
       qn = min(qn, C.L - j0);
+      if (d >= nd || g >= ng || (self && j0 - i0 <= zone)) q0 = qn = 0;  // none / in the zone
+      q0s[g] = q0;
+      qns[g] = qn;
       if (q0 >= qn) continue;
-      double cov;
       if (q0 == 0) {
-        cov = fma(-C.mu[j0], asum, acc[g]);
+        acc[g] = fma(-C.mu[j0], asum, acc[g]);
       } else {  // enters below the first row: direct seed where it starts
         const long long is = i0 + q0, js = j0 + q0;
         const double mis = R.mu[is], mjs = C.mu[js];
         double c0 = 0.0;
         for (int t = 0; t < m; ++t) c0 = fma(R.x[is + t] - mis, C.x[js + t] - mjs, c0);
-        cov = c0;
+        acc[g] = c0;
       }
-      for (long long q = q0; q < qn; ++q) {
-        const long long i = i0 + q, j = j0 + q;
-        if (q > q0) {
-          const double2 ru = R.U[i], cu = C.U[j];
-          cov = fma(ru.x, cu.y, cov);
-          cov = fma(ru.y, cu.x, cov);
+    }
+    __syncwarp();
+    // walk f rows in chunks: the rows' and columns' update vectors and inverse
+    // norms are staged by the warp (one round trip per chunk instead of one
+    // per row), then every lane steps its diagonals through the chunk
+    for (int qc = 0; qc < f; qc += kExpWalk) {
+      for (int q = lane; q < kExpWalk; q += 32) {
+        const long long i = i0 + qc + q;
+        const bool in = i < R.L;
+        S.walk.rU[q] = in ? R.U[i] : make_double2(0.0, 0.0);
+        S.walk.rI[q] = in ? R.inv[i] : 0.0;
+      }
+      for (int q = lane; q < 32 * ng + kExpWalk; q += 32) {
+        const long long j = jbase + d0 + qc + q;
+        const bool in = j >= 0 && j < C.L;
+        S.walk.cU[q] = in ? C.U[j] : make_double2(0.0, 0.0);
+        S.walk.cI[q] = in ? C.inv[j] : 0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int g = 0; g < kExpGroups; ++g) {
+        if (g >= ng) continue;  // warp-uniform
+        const long long q0 = q0s[g], qn = qns[g];
+        const int dl = lane + 32 * g;  // diagonal offset within this block
+        const int qe = min(kExpWalk, f - qc);
+        double cov = acc[g];
+        for (int r = 0; r < qe; ++r) {  // warp-uniform trip count (row i0 + qc + r)
+          const long long q = qc + r;
+          const bool on = q >= q0 && q < qn;
+          if (on && q > q0) {
+            const double2 ru = S.walk.rU[r], cu = S.walk.cU[dl + r];
+            cov = fma(ru.x, cu.y, cov);
+            cov = fma(ru.y, cu.x, cov);
+          }
+          const double ii = S.walk.rI[r], ij = S.walk.cI[dl + r];
+          const bool live = on && ii != 0.0 && ij != 0.0;
+          const double c = cov * (ii * ij);
+          const long long i = i0 + q, j = jbase + d0 + dl + q;
+          if (live) red_min(&PS.keyC[j], mk_key(c, i, imask));
+          // every lane's cell of this row targets keyR[i]: one RED of the warp's minimum
+          long long kr = live ? mk_key(c, j, imask) : kKeyNone;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const long long v = __shfl_xor_sync(0xffffffffu, kr, o);
+            kr = v < kr ? v : kr;
+          }
+          if (lane == 0 && kr != kKeyNone) red_min(&PS.keyR[i], kr);
         }
-        const double ii = R.inv[i], ij = C.inv[j];
-        if (ii == 0.0 || ij == 0.0) continue;
-        const double c = cov * (ii * ij);
-        red_min(&PS.keyR[i], mk_key(c, j, imask));
-        red_min(&PS.keyC[j], mk_key(c, i, imask));
+        acc[g] = cov;
       }
+      __syncwarp();
     }
   }
 }
@@ -1243,36 +1308,6 @@ __global__ void k_fill_keys(long long* __restrict__ k, long long len) {
 }
 
 // ---- K4: finalize --------------------------------------------------------------
-// Exact z-normalised distance between window i of X and window j of Y, one
-// warp: d^2 = m * sum_t ((x_t - mu_i) inv_i - (y_t - mu_j) inv_j)^2.
-__device__ __forceinline__ double warp_exact_dist(const Series& X, long long i, const Series& Y,
-                                                  long long j, int m, int lane) {
-  const double mi = X.mu[i], ii = X.inv[i], mj = Y.mu[j], ij = Y.inv[j];
-  const double* xi = X.x + i;
-  const double* yj = Y.x + j;
-  double acc = 0.0;
-  for (int t = lane; t < m; t += 32) {
-    // rounded products (no FMA contraction): identical windows give exactly 0
-    const double d = __dmul_rn(xi[t] - mi, ii) - __dmul_rn(yj[t] - mj, ij);
-    acc = fma(d, d, acc);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  double d2 = (double)m * acc;
-  const double cap = 4.0 * (double)m;
-  d2 = d2 > cap ? cap : d2;
-  return sqrt(d2);
-}
-
-__device__ __forceinline__ double convention_or_exact(const Series& X, long long i,
-                                                      const Series& Y, long long j, int m,
-                                                      int lane) {
-  const bool fi = X.inv[i] == 0.0, fj = Y.inv[j] == 0.0;
-  if (fi && fj) return 0.0;
-  if (fi || fj) return sqrt((double)m);
-  return warp_exact_dist(X, i, Y, j, m, lane);
-}
-
 // Finalize kernels decode kFinG windows per warp, kFinLanes lanes each: the
 // key loads, the neighbour's statistics and its window of every group are in
 // flight together (one window per warp left each warp waiting on three
@@ -1433,8 +1468,9 @@ __global__ void k_finalize_self_partial(const Series A, const long long* __restr
   }
   const long long best = lk <= rk ? lk : rk;
   const long long bi = best == kKeyNone ? -1 : (best & imask);
-  double v = INFINITY;
-  if (bi >= 0) v = convention_or_exact(A, i, A, bi, m, lane);
+  // every 8-lane group computes the same value, in the same order as the full
+  // join's finalize (so a full-coverage neighbour gets bit-identical values)
+  const double v = group_value(A, i, A, bi, true, m, lane % kFinLanes);
   if (lane == 0) {
     if (mp) mp[i] = v;
     if (pi) pi[i] = bi;

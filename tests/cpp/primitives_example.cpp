@@ -64,14 +64,16 @@ int main(int argc, char **argv) {
     bool same = inplace == ex.distances;
 
     // direct QT of the query with every window, then znorm_dist_from_qt
-    std::vector<double> qt_d(dp.distances.size());
+    std::vector<double> qt_d(dp.distances.size()), qt_raw(dp.distances.size());
     for (std::size_t i = 0; i < qt_d.size(); ++i) {
       double s = 0.0;
       for (mprof::Index k = 0; k < w; ++k) s += query[(std::size_t)k] * ts[(mprof::Index)i + k];
+      qt_raw[i] = s;
       qt_d[i] = mprof::znorm_dist_from_qt(s, w, st.means[(std::size_t)q], st.stds[(std::size_t)q],
                                           st.means[i], st.stds[i]);
     }
     write_vec(out + ".qt", qt_d);
+    write_vec(out + ".qtraw", qt_raw);
 
     mprof::MatrixProfile acc;
     acc.values.assign(dp.distances.size(), mprof::kInf);
