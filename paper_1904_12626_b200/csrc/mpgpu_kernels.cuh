@@ -404,15 +404,14 @@ __device__ __noinline__ SlowOut slow_path(const SlowIn in, unsigned live, int rt
     const double2 ci = S.colI[a];
     if (th > __double2loint(ci.y)) S.colI[a].y = pack_col(ci.x, th);  // lanes of one warp: benign race
   }
-  // row: the lane's best candidate (largest corr, then smallest column), then the warp's
+  // row: the lane's smallest key over its candidates (branch-free), then the warp's
   if (__any_sync(0xffffffffu, rmask != 0)) {
     long long rbest = kKeyNone;
 #pragma unroll
     for (int d = 0; d < kD; ++d) {
-      if ((rmask >> d) & 1u) {
-        const long long key = mk_key(in.c[d], c0 + x0 + d, imask);
-        rbest = key < rbest ? key : rbest;
-      }
+      const long long key = mk_key(in.c[d], c0 + x0 + d, imask);
+      const bool take = ((rmask >> d) & 1u) && key < rbest;
+      rbest = take ? key : rbest;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
