@@ -21,14 +21,39 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def needs_build() -> bool:
-    if not os.path.exists(OUT):
-        return True
-    t = os.path.getmtime(OUT)
+def _deps():
+    inc = os.path.join(ROOT, "include")
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
-    deps += [os.path.join(ROOT, "include", "mprof_gpu.h")]
-    deps += [os.path.join(ROOT, "include", "mprof", f) for f in os.listdir(os.path.join(ROOT, "include", "mprof"))]
-    return any(os.path.getmtime(d) > t for d in deps)
+    deps += [os.path.join(inc, "mprof_gpu.h")]
+    deps += sorted(os.path.join(inc, "mprof", f) for f in os.listdir(os.path.join(inc, "mprof")))
+    deps += [os.path.abspath(__file__)]  # the nvcc command line lives here
+    return deps
+
+
+def source_hash() -> str:
+    """SHA-256 over the tracked sources the library is built from."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in _deps():
+        h.update(os.path.relpath(d, ROOT).encode())
+        with open(d, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+STAMP = OUT + ".stamp"
+
+
+def needs_build() -> bool:
+    """Rebuild unless the .so exists AND its stamp records the hash of exactly
+    the current sources (an untracked or stale binary is never reused)."""
+    if not os.path.exists(OUT) or not os.path.exists(STAMP):
+        return True
+    try:
+        with open(STAMP) as f:
+            return f.read().strip() != source_hash()
+    except OSError:
+        return True
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -47,6 +72,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
         f.write(r.stderr)
     os.replace(OUT + ".tmp", OUT)
+    with open(STAMP, "w") as f:
+        f.write(source_hash() + "\n")
     if verbose:
         print(r.stderr)
     return OUT

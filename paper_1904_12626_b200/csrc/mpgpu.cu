@@ -16,11 +16,22 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "mprof_gpu.h"
 #include "mpgpu_kernels.cuh"
 #include "mpgpu_internal.h"
 
 using namespace mpgpu;
+
+namespace {
+// NVTX range over one host entry point (K1-K5 phases show up by name in
+// nsys / ncu --nvtx timelines; header-only NVTX 3, inert without a tool).
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
+}  // namespace
 
 namespace {
 
@@ -573,6 +584,7 @@ mpgpu_status mpgpu_plan_prepare_finish(mpgpu_plan* p) {
 }
 
 mpgpu_status mpgpu_plan_prepare_shared(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  Range nvtx_range("mpgpu:prepare_shared (K1 stats, coarse prepare)");
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
   if (p->subset) return fail(MPGPU_EUNSUPPORTED, "shared-key joins are full joins");
@@ -623,6 +635,7 @@ mpgpu_status mpgpu_plan_attach_coarse_keys(mpgpu_plan* p, int64_t* d_row_keys, i
 }
 
 mpgpu_status mpgpu_plan_coarse_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  Range nvtx_range("mpgpu:coarse_run (K2b coarse join)");
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (!p->coarse_pending || !p->coarse) return MPGPU_OK;
   MPG_CUDA(cudaSetDevice(p->device));
@@ -633,6 +646,7 @@ mpgpu_status mpgpu_plan_coarse_run(mpgpu_plan* p, int32_t shard, int32_t n_shard
 }
 
 mpgpu_status mpgpu_plan_seed_shared(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  Range nvtx_range("mpgpu:seed_shared (K2 warm start)");
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
   MPG_CUDA(cudaSetDevice(p->device));
@@ -659,6 +673,7 @@ mpgpu_status mpgpu_plan_reset_keys(mpgpu_plan* p) {
 }
 
 mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  Range nvtx_range("mpgpu:prepare (K1 stats, K2 warm start)");
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
   p->coarse_pending = false;
@@ -726,6 +741,7 @@ int64_t mpgpu_plan_shard_cells(const mpgpu_plan* p, int32_t shard, int32_t n_sha
 }
 
 mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
+  Range nvtx_range("mpgpu:run (K3 k_join)");
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
   MPG_CUDA(cudaSetDevice(p->device));
@@ -813,6 +829,7 @@ mpgpu_status mpgpu_plan_finalize(mpgpu_plan* p, double* d_mp_a, int64_t* d_pi_a,
 mpgpu_status mpgpu_plan_finalize_shard(mpgpu_plan* p, int32_t shard, int32_t n_shards,
                                        double* d_mp_a, int64_t* d_pi_a, int64_t* d_left_a,
                                        int64_t* d_right_a, double* d_mp_b, int64_t* d_pi_b) {
+  Range nvtx_range("mpgpu:finalize (K4)");
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
   MPG_CUDA(cudaSetDevice(p->device));
@@ -1250,6 +1267,7 @@ mpgpu_status mpgpu_ipc_close(void* d_ptr, int32_t device) {
 
 mpgpu_status mpgpu_keys_min_merge(int64_t* d_dst, const int64_t* d_src, int64_t len,
                                   int32_t device, void* cuda_stream) {
+  Range nvtx_range("mpgpu:keys_min (K5)");
   MPG_CUDA(cudaSetDevice(device));
   if (len <= 0) return MPGPU_OK;
   k_keys_min<<<(unsigned)((len + 255) / 256), 256, 0, (cudaStream_t)cuda_stream>>>(
@@ -1395,6 +1413,7 @@ mpgpu_status ctx_plan(DevCtx* c, const mpgpu_join_args* a) {
 
 mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* total_ms,
                        const std::vector<int64_t>* band_ids = nullptr) {
+  Range nvtx_range("mpgpu:join (host buffers)");
   const auto t0 = std::chrono::steady_clock::now();
   if (!a || !a->a) return fail(MPGPU_EPARAM, "null arguments");
   const bool self = a->b == nullptr;
