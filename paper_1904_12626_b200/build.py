@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libmprof_b200.so")
-SOURCES = ["mpgpu.cu", "mpgpu_multi.cu", "mpgpu_stripes.cpp", "mprof_api.cpp"]
+SOURCES = ["mpgpu.cu", "mpgpu_multi.cu", "mpgpu_stripes.cpp", "mprof_api.cpp", "mprof_archive.cpp"]
 HEADERS = ["mpgpu_kernels.cuh", "mpgpu_internal.h"]
 
 
