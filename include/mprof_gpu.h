@@ -82,18 +82,32 @@ mpgpu_status mpgpu_join(const mpgpu_join_args *args);
  * the whole call including host<->device copies, in milliseconds. */
 mpgpu_status mpgpu_join_timed(const mpgpu_join_args *args, double *kernel_ms, double *total_ms);
 
-/* SCRIMP (profile.hpp:85-89) with the anytime property: a self-join over a
- * seeded random subset of diagonal bands (kW = 256 consecutive diagonals each)
- * covering at least s_size diagonals; s_size <= 0 or >= all diagonals is the
- * full exact join. *coverage = diagonals computed / all diagonals. Below full
- * coverage left_a / right_a come back as -1 and values are the
- * exact minima over the computed diagonals (element-wise upper bounds of the
- * full profile). AB-joins -> MPGPU_EUNSUPPORTED. */
+/* SCRIMP (profile.hpp:85-89) with the anytime property: a
+ * self-join over exactly s_size diagonals taken in SCRIMP's seeded order
+ * (Fisher-Yates over the admissible diagonals, splitmix64 from `seed`;
+ * mpgpu_scrimp_diagonals lists them), each evaluated in full by k_diag_join.
+ * s_size <= 0 or >= all diagonals is the full exact join. *coverage =
+ * s_size / all diagonals exactly. Below full coverage left_a / right_a come
+ * back as -1 and values are the exact minima over the computed
+ * diagonals (element-wise upper bounds of the full profile). AB-joins ->
+ * MPGPU_EUNSUPPORTED. */
 mpgpu_status mpgpu_scrimp(const mpgpu_join_args *args, int64_t s_size, uint64_t seed,
                           double *coverage);
 
-/* The band subset mpgpu_scrimp evaluates for (n, window, zone, s_size, seed):
- * writes up to `cap` band ids (ascending; band b = diagonals
+/* The diagonals mpgpu_scrimp evaluates for (n, window, zone, s_size, seed):
+ * writes up to `cap` of them (ascending) and returns how many there are. */
+int64_t mpgpu_scrimp_diagonals(int64_t n, int64_t window, int64_t zone, int64_t s_size,
+                               uint64_t seed, int64_t *out_diags, int64_t cap, double *coverage);
+
+/* The band-granular fast path of anytime SCRIMP: whole bands of kW = 256
+ * consecutive diagonals chosen in a seeded order until at least s_size
+ * diagonals are covered, evaluated by the full join kernel (k_join). Same
+ * outputs and conventions as mpgpu_scrimp; *coverage = covered / all. */
+mpgpu_status mpgpu_scrimp_banded(const mpgpu_join_args *args, int64_t s_size, uint64_t seed,
+                                 double *coverage);
+
+/* The band subset mpgpu_scrimp_banded evaluates for (n, window, zone, s_size,
+ * seed): writes up to `cap` band ids (ascending; band b = diagonals
  * [zone+1 + 256 b, zone+1 + 256 (b+1))) and returns how many there are. */
 int64_t mpgpu_scrimp_bands(int64_t n, int64_t window, int64_t zone, int64_t s_size, uint64_t seed,
                            int64_t *out_bands, int64_t cap, double *coverage);

@@ -140,6 +140,10 @@ def lib() -> ctypes.CDLL:
     L.mpgpu_scrimp.restype = ctypes.c_int
     L.mpgpu_scrimp_bands.argtypes = [ctypes.c_int64] * 4 + [ctypes.c_uint64, _ip, ctypes.c_int64, _dp]
     L.mpgpu_scrimp_bands.restype = ctypes.c_int64
+    L.mpgpu_scrimp_diagonals.argtypes = [ctypes.c_int64] * 4 + [ctypes.c_uint64, _ip, ctypes.c_int64, _dp]
+    L.mpgpu_scrimp_diagonals.restype = ctypes.c_int64
+    L.mpgpu_scrimp_banded.argtypes = [ctypes.POINTER(_JoinArgs), ctypes.c_int64, ctypes.c_uint64, _dp]
+    L.mpgpu_scrimp_banded.restype = ctypes.c_int
     L.mpgpu_plan_select_bands.argtypes = [ctypes.c_void_p, _ip, ctypes.c_int64]
     L.mpgpu_plan_select_bands.restype = ctypes.c_int
     L.mpgpu_distance_profiles.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64,
@@ -415,6 +419,17 @@ def scrimp_bands(n: int, window: int, zone: int, s_size: int, seed: int = 0):
     return out[:k].copy(), cov.value
 
 
+def scrimp_diagonals(n: int, window: int, zone: int, s_size: int, seed: int = 0):
+    """(diagonals ascending, coverage) that scrimp(granularity="diagonal") evaluates."""
+    L = n - window + 1
+    cap = max(1, L - zone - 1)
+    out = np.empty(cap, dtype=np.int64)
+    cov = ctypes.c_double(0)
+    k = lib().mpgpu_scrimp_diagonals(n, window, zone, s_size, ctypes.c_uint64(seed), _ptr(out, _ip), cap,
+                                     ctypes.byref(cov))
+    return out[:k].copy(), cov.value
+
+
 def band_diagonals(bands, L: int, zone: int) -> np.ndarray:
     """Explicit diagonal list of a band subset."""
     parts = [np.arange(zone + 1 + b * BAND, min(zone + 1 + (b + 1) * BAND, L)) for b in bands]
@@ -423,15 +438,19 @@ def band_diagonals(bands, L: int, zone: int) -> np.ndarray:
 
 def scrimp(ts_a, window: int = 4, ez_fraction: float = 0.5, s_size: int = K_FULL_RUN,
            seed: int = 0, progress: Optional[Callable[[float], None]] = None,
-           ts_b=None) -> MatrixProfile:
+           ts_b=None, granularity: str = "diagonal") -> MatrixProfile:
     """mprof::scrimp (profile.hpp:85-89): self-join with the anytime property.
 
-    s_size diagonals (rounded up to whole 256-diagonal bands, chosen in a
-    seeded random order) are evaluated; coverage = computed / all diagonals.
+    granularity="diagonal" (the reference's semantics): exactly s_size
+    diagonals in SCRIMP's seeded order (scrimp_diagonals), coverage =
+    s_size / all diagonals. granularity="band": the fast path, whole
+    256-diagonal bands in a seeded order until s_size diagonals are covered.
     At full coverage the result is the exact join with left/right indexes;
     below it values are exact minima over the computed diagonals and
     left/right are absent. AB-joins raise
     UnsupportedError (SPEC.md:219)."""
+    if granularity not in ("diagonal", "band"):
+        raise ParameterError("granularity must be 'diagonal' or 'band'")
     if ts_b is not None:
         raise UnsupportedError("SCRIMP supports self-joins only")
     if s_size < 1:
@@ -459,7 +478,8 @@ def scrimp(ts_a, window: int = 4, ez_fraction: float = 0.5, s_size: int = K_FULL
     args.mp_a, args.pi_a = _ptr(mp_a, _dp), _ptr(pi_a, _ip)
     args.left_a, args.right_a = _ptr(left, _ip), _ptr(right, _ip)
     cov = ctypes.c_double(0)
-    _check(lib().mpgpu_scrimp(ctypes.byref(args), int(s_size), ctypes.c_uint64(seed), ctypes.byref(cov)))
+    fn = lib().mpgpu_scrimp if granularity == "diagonal" else lib().mpgpu_scrimp_banded
+    _check(fn(ctypes.byref(args), int(s_size), ctypes.c_uint64(seed), ctypes.byref(cov)))
     full = cov.value >= 1.0
     return MatrixProfile(values=mp_a, index=pi_a,
                          left_index=left if full else np.empty(0, np.int64),

@@ -134,6 +134,13 @@ struct mpgpu_plan {
   bool subset = false;
   long long* d_init_diags = nullptr;  // anytime warm start: diagonals inside the chosen bands
   int n_init_diags = 0;
+  // anytime (SCRIMP) over an explicit diagonal set: k_diag_join instead of k_join
+  bool diag_mode = false;
+  long long* d_diags = nullptr;
+  long long n_diags = 0;
+  DiagItem* d_ditems = nullptr;
+  int n_ditems = 0;
+  int diag_rows = 0;
   // keys owned by another plan (possibly on a peer device, reached over NVLink):
   // this plan's k_join reads thresholds from and RED.MINs into them directly
   long long* ext_key0 = nullptr;
@@ -555,6 +562,8 @@ void mpgpu_plan_destroy(mpgpu_plan* p) {
   cudaFree(p->d_counter);
   cudaFree(p->d_bands);
   cudaFree(p->d_init_diags);
+  cudaFree(p->d_diags);
+  cudaFree(p->d_ditems);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -745,6 +754,20 @@ mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
   if (!p) return fail(MPGPU_EPARAM, "null plan");
   if (n_shards < 1 || shard < 0 || shard >= n_shards) return fail(MPGPU_EPARAM, "bad shard");
   MPG_CUDA(cudaSetDevice(p->device));
+  if (p->diag_mode) {
+    if (n_shards != 1) return fail(MPGPU_EUNSUPPORTED, "diagonal-subset runs are not sharded");
+    if (p->n_ditems == 0) return MPGPU_OK;
+    MPG_CUDA(cudaMemsetAsync(p->d_counter, 0, sizeof(int), p->stream));
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+    const int grid = (int)std::min<long long>((p->n_ditems + 7) / 8, (long long)sms * 8);
+    k_diag_join<<<grid, 256, 0, p->stream>>>(p->A.view(), key_row(p), key_col(p), p->d_diags,
+                                             p->n_diags, p->d_ditems, p->n_ditems, p->d_counter,
+                                             p->diag_rows, (int)p->m, p->imask);
+    p->launches += 1;
+    MPG_CUDA(cudaGetLastError());
+    return MPGPU_OK;
+  }
   // each shard uses its own slice of the device item buffer (shards may be
   // in flight together on one device); a slice is uploaded on its first run
   // and reused while the sharding and the band selection stay the same
@@ -841,7 +864,14 @@ mpgpu_status mpgpu_plan_finalize_shard(mpgpu_plan* p, int32_t shard, int32_t n_s
   };
   auto grid = [&](long long nrows) { return (unsigned)((nrows * kFinLanes + bs - 1) / bs); };
   long long r0, r1;
-  if (p->self && p->subset) {
+  if (p->diag_mode) {
+    if (n_shards != 1) return fail(MPGPU_EUNSUPPORTED, "anytime runs finalize in one piece");
+    k_finalize_keys<<<grid(p->A.L), bs, 0, p->stream>>>(p->A.view(), key_row(p), key_col(p),
+                                                         (int)p->m, p->imask, d_mp_a,
+                                                         (long long*)d_pi_a, (long long*)d_left_a,
+                                                         (long long*)d_right_a);
+    p->launches += 1;
+  } else if (p->self && p->subset) {
     if (n_shards != 1) return fail(MPGPU_EUNSUPPORTED, "anytime runs finalize in one piece");
     const long long thr = p->A.L * 32;
     k_finalize_self_partial<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
@@ -1006,9 +1036,11 @@ mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int
   if (n < 0 || !band_ids) {  // back to the full join
     if (p->subset) p->slice_n = 0;
     p->subset = false;
+    p->diag_mode = false;
     p->bands.clear();
     return MPGPU_OK;
   }
+  p->diag_mode = false;
   if (!p->self) return fail(MPGPU_EUNSUPPORTED, "band subsets (anytime SCRIMP) are self-join only");
   const long long nb = mpgpu_plan_num_bands(p), klo = p->zone + 1;
   std::vector<long long> kb;
@@ -1049,6 +1081,105 @@ mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int
   p->subset = true;
   p->slice_n = 0;  // item order changed: re-upload on the next run
   return MPGPU_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// Anytime mode over an explicit diagonal set (ascending, > zone, < L): work
+// items are 32 consecutive diagonals x a segment of rows, largest first; the
+// warm start uses up to kInitDiag diagonals spread over the set.
+mpgpu_status plan_select_diagonals(mpgpu_plan* p, const std::vector<long long>& diags) {
+  if (!p->self) return fail(MPGPU_EUNSUPPORTED, "diagonal subsets (anytime SCRIMP) are self-join only");
+  MPG_CUDA(cudaSetDevice(p->device));
+  const long long L = p->A.L;
+  cudaFree(p->d_diags);
+  cudaFree(p->d_ditems);
+  p->d_diags = nullptr;
+  p->d_ditems = nullptr;
+  p->n_diags = (long long)diags.size();
+  // rows per item: long enough that the m-term seed is small against the walk
+  // (>= 8m), short enough to spread the set over every warp
+  const long long groups = (p->n_diags + 31) / 32;
+  long long cells = 0;
+  for (long long k : diags) cells += L - k;
+  const long long workers = 148LL * 64;
+  long long rows = std::max<long long>(8 * p->m, cells / std::max<long long>(1, 32 * 4 * workers));
+  rows = std::max<long long>(256, std::min<long long>(rows, 1 << 20));
+  p->diag_rows = (int)rows;
+  std::vector<std::pair<long long, DiagItem>> its;
+  for (long long g = 0; g < groups; ++g) {
+    const long long kmin = diags[(size_t)(g * 32)];  // ascending: the group's longest diagonal
+    const long long nrows = L - kmin;
+    for (long long s0 = 0; s0 * rows < nrows; ++s0) {
+      DiagItem it;
+      it.group = (int)g;
+      it.seg = (int)s0;
+      its.push_back({std::min(rows, nrows - s0 * rows), it});
+    }
+  }
+  std::stable_sort(its.begin(), its.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+  std::vector<DiagItem> h(its.size());
+  for (size_t q = 0; q < its.size(); ++q) h[q] = its[q].second;
+  p->n_ditems = (int)h.size();
+  if (!diags.empty()) {
+    MPG_CUDA(cudaMalloc(&p->d_diags, sizeof(long long) * diags.size()));
+    MPG_CUDA(cudaMemcpy(p->d_diags, diags.data(), sizeof(long long) * diags.size(),
+                        cudaMemcpyHostToDevice));
+  }
+  if (!h.empty()) {
+    MPG_CUDA(cudaMalloc(&p->d_ditems, sizeof(DiagItem) * h.size()));
+    MPG_CUDA(cudaMemcpy(p->d_ditems, h.data(), sizeof(DiagItem) * h.size(), cudaMemcpyHostToDevice));
+  }
+  std::vector<long long> wd;
+  const int nw = (int)std::min<size_t>(kInitDiag, diags.size());
+  for (int q = 0; q < nw; ++q) {
+    const long long k = diags[(size_t)q * diags.size() / nw];
+    if (wd.empty() || wd.back() != k) wd.push_back(k);
+  }
+  cudaFree(p->d_init_diags);
+  p->d_init_diags = nullptr;
+  p->n_init_diags = 0;
+  if (!wd.empty()) {
+    MPG_CUDA(cudaMalloc(&p->d_init_diags, sizeof(long long) * wd.size()));
+    MPG_CUDA(cudaMemcpy(p->d_init_diags, wd.data(), sizeof(long long) * wd.size(),
+                        cudaMemcpyHostToDevice));
+    p->n_init_diags = (int)wd.size();
+  }
+  p->bands.clear();
+  p->subset = true;
+  p->diag_mode = true;
+  p->slice_n = 0;
+  return MPGPU_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int64_t mpgpu_scrimp_diagonals(int64_t n, int64_t window, int64_t zone, int64_t s_size,
+                               uint64_t seed, int64_t* out_diags, int64_t cap, double* coverage) {
+  const long long L = n - window + 1, klo = zone + 1;
+  const long long nd = L > klo ? L - klo : 0;
+  // SCRIMP's seeded diagonal order: Fisher-Yates over the
+  // admissible diagonals with splitmix64, the first s_size of them
+  std::vector<long long> order((size_t)nd);
+  for (long long q = 0; q < nd; ++q) order[(size_t)q] = klo + q;
+  uint64_t st = seed;
+  auto next = [&st]() {
+    uint64_t z = (st += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  };
+  for (long long q = nd - 1; q > 0; --q) {
+    const long long r = (long long)(next() % (uint64_t)(q + 1));
+    std::swap(order[(size_t)q], order[(size_t)r]);
+  }
+  const long long take = (s_size <= 0 || s_size >= nd) ? nd : s_size;
+  std::sort(order.begin(), order.begin() + take);
+  for (long long q = 0; q < take && q < cap; ++q) out_diags[q] = order[(size_t)q];
+  if (coverage) *coverage = nd > 0 ? (double)take / (double)nd : 1.0;
+  return take;
 }
 
 int64_t mpgpu_scrimp_bands(int64_t n, int64_t window, int64_t zone, int64_t s_size, uint64_t seed,
@@ -1412,7 +1543,8 @@ mpgpu_status ctx_plan(DevCtx* c, const mpgpu_join_args* a) {
 }
 
 mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* total_ms,
-                       const std::vector<int64_t>* band_ids = nullptr) {
+                       const std::vector<int64_t>* band_ids = nullptr,
+                       const std::vector<long long>* diag_ids = nullptr) {
   Range nvtx_range("mpgpu:join (host buffers)");
   const auto t0 = std::chrono::steady_clock::now();
   if (!a || !a->a) return fail(MPGPU_EPARAM, "null arguments");
@@ -1421,7 +1553,7 @@ mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* tota
   if (a->window > a->n_a || (!self && a->window > a->n_b))
     return fail(MPGPU_EPARAM, "series shorter than the window");
   if (a->zone < 0) return fail(MPGPU_EPARAM, "negative exclusion zone");
-  const int ng = a->n_gpus > 0 ? a->n_gpus : 1;
+  const int ng = diag_ids ? 1 : (a->n_gpus > 0 ? a->n_gpus : 1);  // subsets: one device
   std::vector<int> devs(ng);
   for (int g = 0; g < ng; ++g) devs[g] = a->devices ? a->devices[g] : g;
   const long long La = a->n_a - a->window + 1;
@@ -1447,8 +1579,9 @@ mpgpu_status join_impl(const mpgpu_join_args* a, double* kernel_ms, double* tota
     if (!self) MPG_CUDA(c->xb.ensure(sizeof(double) * a->n_b));
     st = ctx_plan(c, a);
     if (st != MPGPU_OK) return st;
-    st = band_ids ? mpgpu_plan_select_bands(c->plan, band_ids->data(), (int64_t)band_ids->size())
-                  : mpgpu_plan_select_bands(c->plan, nullptr, -1);
+    st = diag_ids ? plan_select_diagonals(c->plan, *diag_ids)
+         : band_ids ? mpgpu_plan_select_bands(c->plan, band_ids->data(), (int64_t)band_ids->size())
+                    : mpgpu_plan_select_bands(c->plan, nullptr, -1);
     if (st != MPGPU_OK) return st;
   }
   DevCtx* c0 = ctx[0];
@@ -1673,6 +1806,25 @@ mpgpu_status mpgpu_mass_host(const double* query, int64_t window, const double* 
 
 mpgpu_status mpgpu_scrimp(const mpgpu_join_args* args, int64_t s_size, uint64_t seed,
                           double* coverage) {
+  if (!args || !args->a) return fail(MPGPU_EPARAM, "null arguments");
+  if (args->b) return fail(MPGPU_EUNSUPPORTED, "SCRIMP supports self-joins only");
+  if (args->window < 4 || args->window > args->n_a)
+    return fail(MPGPU_EPARAM, "window out of range");
+  if (args->zone < 0) return fail(MPGPU_EPARAM, "negative exclusion zone");
+  const long long L = args->n_a - args->window + 1;
+  const long long nd = L > args->zone + 1 ? L - args->zone - 1 : 0;
+  std::vector<int64_t> ids((size_t)std::max<long long>(nd, 1));
+  double cov = 1.0;
+  const int64_t n = mpgpu_scrimp_diagonals(args->n_a, args->window, args->zone, s_size, seed,
+                                           ids.data(), (int64_t)ids.size(), &cov);
+  if (coverage) *coverage = cov;
+  if (cov >= 1.0) return join_impl(args, nullptr, nullptr);  // full coverage: exact join
+  std::vector<long long> diags(ids.begin(), ids.begin() + n);
+  return join_impl(args, nullptr, nullptr, nullptr, &diags);
+}
+
+mpgpu_status mpgpu_scrimp_banded(const mpgpu_join_args* args, int64_t s_size, uint64_t seed,
+                                 double* coverage) {
   if (!args || !args->a) return fail(MPGPU_EPARAM, "null arguments");
   if (args->b) return fail(MPGPU_EUNSUPPORTED, "SCRIMP supports self-joins only");
   if (args->window < 4 || args->window > args->n_a)

@@ -705,6 +705,92 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
   }
 }
 
+// ---- K3d: anytime join over an explicit diagonal set (SCRIMP, exact s_size) ------
+// SCRIMP evaluates s_size diagonals in a seeded order. The
+// band kernel above needs 256 consecutive diagonals per warp; a random subset
+// has no such runs, so this kernel gives every lane its own diagonal: a warp
+// takes 32 consecutive entries of the sorted subset and a segment of rows.
+// Each lane seeds its covariance by a direct centred dot product, then walks
+// its rows with the join's recurrence. Row data are warp-broadcast loads;
+// column data are per-lane sequential loads. Flat windows take the
+// convention in-kernel (both flat: distance 0, one flat: sqrt(m)), so the
+// keys are complete and the finalize only decodes them. Exact (no filter
+// quantisation): a cell updates a key only when its packed key is smaller.
+struct DiagItem {
+  int group;  // diagonals diags[32 group + lane]
+  int seg;    // rows [seg * rows, (seg + 1) * rows)
+};
+
+__global__ void __launch_bounds__(256) k_diag_join(const Series A, long long* __restrict__ keyR,
+                                                   long long* __restrict__ keyC,
+                                                   const long long* __restrict__ diags,
+                                                   long long n_diags, const DiagItem* __restrict__ items,
+                                                   int n_items, int* __restrict__ counter, int rows,
+                                                   int m, long long imask) {
+  const int lane = threadIdx.x & 31;
+  const double half_corr = 0.5;  // one flat window: d = sqrt(m) -> corr = 1 - d^2 / 2m = 1/2
+  for (;;) {
+    int id = 0;
+    if (lane == 0) id = atomicAdd(counter, 1);
+    id = __shfl_sync(0xffffffffu, id, 0);
+    if (id >= n_items) break;
+    const DiagItem it = items[id];
+    const long long q = (long long)it.group * 32 + lane;
+    const long long k = q < n_diags ? diags[q] : -1;
+    const long long r0 = (long long)it.seg * rows;
+    // rows of this lane: [r0, r1) with j = i + k < L
+    const long long r1 = k >= 0 ? min(r0 + rows, A.L - k) : r0;
+    double cov = 0.0;
+    if (r1 > r0) {
+      const double mi = A.mu[r0], mj = A.mu[r0 + k];
+      const double* xi = A.x + r0;
+      const double* xj = A.x + r0 + k;
+      for (int t = 0; t < m; ++t) cov = fma(xi[t] - mi, xj[t] - mj, cov);
+    }
+    // the warp walks the longest lane's rows; shorter lanes idle at the end
+    long long rmax = r1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    for (long long i = r0; i < rmax; ++i) {
+      const bool on = i < r1;
+      const long long j = i + (on ? k : 0);
+      const double2 ru = A.U[i];
+      const double ri = A.inv[i];
+      long long kr = kKeyNone;
+      if (on) {
+        if (i > r0) {
+          const double2 cu = A.U[j];
+          cov = fma(ru.x, cu.y, cov);
+          cov = fma(ru.y, cu.x, cov);
+        }
+        const double cj = A.inv[j];
+        const bool fi = ri == 0.0, fj = cj == 0.0;
+        const double c = (fi && fj) ? 1.0 : ((fi || fj) ? half_corr : cov * (ri * cj));
+        const long long kc = mk_key(c, i, imask);
+        if (kc < keyC[j]) red_min(&keyC[j], kc);
+        kr = mk_key(c, j, imask);
+      }
+      const long long cur = keyR[i];  // same address for every lane: one broadcast load
+      if (__any_sync(0xffffffffu, kr < cur)) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const long long v = __shfl_xor_sync(0xffffffffu, kr, o);
+          kr = v < kr ? v : kr;
+        }
+        if (lane == 0 && kr < cur) red_min(&keyR[i], kr);
+      }
+    }
+  }
+}
+
+// Decode keys that are complete (the diagonal-subset join): value at the
+// best of the left / right keys, exact distance or flat convention; left /
+// right indexes are not part of a partial result.
+__global__ void k_finalize_keys(const Series A, const long long* __restrict__ key_right,
+                                const long long* __restrict__ key_left, int m, long long imask,
+                                double* __restrict__ mp, long long* __restrict__ pi,
+                                long long* __restrict__ left, long long* __restrict__ right);
+
 // ---- K2: warm-start keys -------------------------------------------------------
 // Every row and column gets a real candidate before the join, so the join's
 // filter never runs against an empty key (an empty key makes every warp that
@@ -1475,6 +1561,26 @@ __global__ void k_finalize_self_partial(const Series A, const long long* __restr
     if (pi) pi[i] = bi;
     if (left) left[i] = -1;
     if (right) right[i] = -1;
+  }
+}
+
+__global__ void k_finalize_keys(const Series A, const long long* __restrict__ key_right,
+                                const long long* __restrict__ key_left, int m, long long imask,
+                                double* __restrict__ mp, long long* __restrict__ pi,
+                                long long* __restrict__ left, long long* __restrict__ right) {
+  const long long gi = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / kFinLanes;
+  const int sub = threadIdx.x % kFinLanes;
+  const bool valid = gi < A.L;
+  const long long ic = valid ? gi : 0;
+  const long long rk = key_right[ic], lk = key_left[ic];
+  const long long best = lk <= rk ? lk : rk;
+  const long long bi = best == kKeyNone ? -1 : (best & imask);
+  const double v = group_value(A, ic, A, bi, valid, m, sub);
+  if (valid && sub == 0) {
+    if (mp) mp[gi] = v;
+    if (pi) pi[gi] = bi;
+    if (left) left[gi] = -1;
+    if (right) right[gi] = -1;
   }
 }
 

@@ -86,19 +86,21 @@ def test_cpp_errors_map_to_reference_exceptions(exe, tmp_path):
 
 
 def test_cpp_scrimp_anytime(exe, tmp_path, oracle_lib):
-    """mprof::scrimp with s_size (profile.hpp:87-89): a seeded band subset, coverage < 1,
-    left/right empty, values equal the oracle's SCRIMP over exactly those diagonals."""
+    """mprof::scrimp with s_size (profile.hpp:87-89; SPEC.md:218-223): exactly
+    s_size diagonals in SCRIMP's seeded order, coverage = s_size / all
+    diagonals, left/right empty, values equal the oracle's own SCRIMP run."""
     import paper_1904_12626_b200 as mp
     x = np.cumsum(np.random.default_rng(12).standard_normal(20000))
     w, ez, seed = 64, 0.5, 4
     zone = mp.zone_size(w, ez)
     L = x.size - w + 1
-    s_size = (L - zone - 1) // 5
+    nd = L - zone - 1
+    s_size = nd // 5
     rc, info, res = _run(exe, tmp_path, x, w, ez, "anytime", extra=(s_size, seed))
-    bands, cov = mp.scrimp_bands(x.size, w, zone, s_size, seed)
-    assert rc == 0 and info["mode"] == "scrimp" and abs(info["coverage"] - cov) < 1e-15 and cov < 1.0
+    assert rc == 0 and info["mode"] == "scrimp" and info["coverage"] == s_size / nd
     assert res["left"].size == 0 and res["right"].size == 0
-    ref_mp, ref_pi = oracle_lib.scrimp_diagonals(x, w, mp.band_diagonals(bands, L, zone))
+    ref_mp, ref_pi, _, _, ref_cov = oracle_lib.scrimp(x, w, ez, s_size=s_size, seed=seed)
+    assert ref_cov == info["coverage"]
     assert close(res["mp"], ref_mp)[0]
     assert not index_mismatches(res["pi"], ref_pi, np.arange(L), x, x, w)
 

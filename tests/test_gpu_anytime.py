@@ -1,7 +1,12 @@
-"""Anytime SCRIMP (profile.hpp:85-89) on the GPU: a seeded
-subset of 256-diagonal bands, checked against the oracle's SCRIMP loop over
-exactly those diagonals, plus the anytime contract (coverage, monotonicity,
-left/right absent below full coverage, full coverage == the exact join)."""
+"""Anytime SCRIMP (profile.hpp:85-89) on the GPU.
+
+Exact mode (the reference's semantics, the default): exactly s_size
+diagonals in SCRIMP's seeded order, checked against the oracle's own
+or_scrimp with the same s_size and seed (same diagonal order), coverage ==
+s_size / all diagonals. Band mode (the fast path): a seeded subset of
+256-diagonal bands, checked against the oracle's SCRIMP loop over exactly
+those diagonals. Plus the anytime contract (monotonicity, left/right absent
+below full coverage, full coverage == the exact join) in both modes."""
 import numpy as np
 import pytest
 
@@ -21,7 +26,7 @@ def mp():
 
 
 def _check_subset(mp, oracle_lib, x, w, ez, s_size, seed):
-    r = mp.scrimp(x, w, ez, s_size=s_size, seed=seed)
+    r = mp.scrimp(x, w, ez, s_size=s_size, seed=seed, granularity="band")
     zone = mp.zone_size(w, ez)
     L = x.size - w + 1
     bands, cov = mp.scrimp_bands(x.size, w, zone, s_size, seed)
@@ -58,15 +63,53 @@ def test_anytime_with_flat_runs(mp, oracle_lib):
     _check_subset(mp, oracle_lib, y, 32, 0.5, nd // 2, 6)
 
 
-def test_anytime_monotone_and_full(mp):
+@pytest.mark.parametrize("gran", ["band", "diagonal"])
+def test_anytime_monotone_and_full(mp, gran):
     x = np.cumsum(np.random.default_rng(33).standard_normal(20000))
     w, ez = 100, 0.5
     nd = x.size - w + 1 - mp.zone_size(w, ez) - 1
-    r1 = mp.scrimp(x, w, ez, s_size=nd // 20, seed=9)
-    r2 = mp.scrimp(x, w, ez, s_size=nd // 4, seed=9)
-    full = mp.scrimp(x, w, ez, seed=9)
+    r1 = mp.scrimp(x, w, ez, s_size=nd // 20, seed=9, granularity=gran)
+    r2 = mp.scrimp(x, w, ez, s_size=nd // 4, seed=9, granularity=gran)
+    full = mp.scrimp(x, w, ez, seed=9, granularity=gran)
     st = mp.stomp(x, None, w, ez)
     assert r1.coverage < r2.coverage < full.coverage == 1.0
     assert np.all(r2.values <= r1.values) and np.all(full.values <= r2.values)
     assert np.array_equal(full.values, st.values) and np.array_equal(full.index, st.index)
     assert np.array_equal(full.left_index, st.left_index) and full.has_left_right()
+
+
+@pytest.mark.parametrize("n,w,ez,frac,seed", [(30000, 64, 0.5, 0.1, 1), (12000, 50, 0.25, 0.37, 5),
+                                             (5000, 32, 0.5, 1e-4, 3), (40000, 128, 0.5, 0.02, 11)])
+def test_exact_mode_matches_oracle_scrimp(mp, oracle_lib, n, w, ez, frac, seed):
+    """The reference's SCRIMP semantics: the GPU evaluates exactly the oracle's
+    first s_size diagonals of the seeded order (s_size = 1 included), so the
+    partial profiles agree with or_scrimp itself; coverage is s_size / total."""
+    g = np.random.default_rng(seed)
+    x = np.cumsum(g.standard_normal(n))
+    x[n // 5:n // 5 + 3 * w] = x[n // 5]      # a flat run: the convention inside the subset
+    x[n // 2:n // 2 + w] = 2.0
+    zone = mp.zone_size(w, ez)
+    L = n - w + 1
+    nd = L - zone - 1
+    s_size = max(1, int(nd * frac))
+    r = mp.scrimp(x, w, ez, s_size=s_size, seed=seed)
+    assert r.coverage == s_size / nd and not r.has_left_right()
+    diags, cov = mp.scrimp_diagonals(n, w, zone, s_size, seed)
+    assert diags.size == s_size and cov == r.coverage and np.all(diags > zone)
+    ref_mp, ref_pi, _, _, ref_cov = oracle_lib.scrimp(x, w, ez, s_size=s_size, seed=seed)
+    assert ref_cov == r.coverage
+    ok, rel = close(r.values, ref_mp)
+    assert ok, f"exact anytime MP mismatch (max rel {rel:.3e})"
+    assert np.array_equal(np.isinf(r.values), np.isinf(ref_mp))
+    assert not index_mismatches(r.index, ref_pi, np.arange(L), x, x, w)
+    # every reported neighbour sits on a chosen diagonal
+    fin = r.index >= 0
+    assert np.isin(np.abs(r.index[fin] - np.arange(L)[fin]), diags).all()
+
+
+def test_exact_mode_via_cpp_default(mp, oracle_lib):
+    """mprof::scrimp through the C ABI default (mpgpu_scrimp) is the exact mode."""
+    x = np.cumsum(np.random.default_rng(7).standard_normal(8000))
+    r = mp.scrimp(x, 40, 0.5, s_size=777, seed=2)
+    ref_mp = oracle_lib.scrimp(x, 40, 0.5, s_size=777, seed=2)[0]
+    assert close(r.values, ref_mp)[0] and r.coverage == 777 / (8000 - 40 + 1 - 20 - 1)
