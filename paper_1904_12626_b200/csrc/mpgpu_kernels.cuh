@@ -26,10 +26,10 @@ namespace mpgpu {
 #endif
 constexpr int kD = MPGPU_D;                // diagonals per thread (register block)
 #ifndef MPGPU_WARPS
-#define MPGPU_WARPS 8
+#define MPGPU_WARPS 12
 #endif
 #ifndef MPGPU_MINBLOCKS
-#define MPGPU_MINBLOCKS 2
+#define MPGPU_MINBLOCKS 1
 #endif
 constexpr int kMinBlocks = MPGPU_MINBLOCKS;  // CTAs per SM the register budget targets
 #ifndef MPGPU_BLOCK
@@ -539,11 +539,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
     }
 
     // ---- tile 0: rows [0, kH) -> buffer 0, columns [0, kH + kW - 1) ------
-    static_assert(kH <= 32, "one row / column per lane per tile");
-    if (lane < kH) fetch_row(S, PS, 0, lane, r0 + lane);
+    static_assert(kH >= 1, "tile rows");
+    if constexpr (kH <= 32) {
+      if (lane < kH) fetch_row(S, PS, 0, lane, r0 + lane);
+    } else {
+      for (int h = lane; h < kH; h += 32) fetch_row(S, PS, 0, h, r0 + h);
+    }
     for (int x = lane; x < kH + kW - 1; x += 32) fetch_col(S, PS, c0, x);
     cp_async_wait_all();
-    if (lane < kH) fix_row(S, PS, 0, lane, r0 + lane, imask);
+    if constexpr (kH <= 32) {
+      if (lane < kH) fix_row(S, PS, 0, lane, r0 + lane, imask);
+    } else {
+      for (int h = lane; h < kH; h += 32) fix_row(S, PS, 0, h, r0 + h, imask);
+    }
     if (lane == 0) S.rowU[0][0] = make_double2(0.0, 0.0);  // the seed row takes no step
     for (int x = lane; x < kH + kW - 1; x += 32) fix_col(S, PS, c0, x, imask);
     __syncwarp();
@@ -561,9 +569,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       const int buf = t & 1;
       const long long ts = (long long)t * kH;
       // ---- prefetch tile t+1 (its ring slots held columns retired by now) ----
-      if (t + 1 < nT && lane < kH) {
-        fetch_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane);
-        fetch_col(S, PS, c0, ts + kH + kW - 1 + lane);
+      if constexpr (kH <= 32) {
+        if (t + 1 < nT && lane < kH) {
+          fetch_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane);
+          fetch_col(S, PS, c0, ts + kH + kW - 1 + lane);
+        }
+      } else if (t + 1 < nT) {
+#pragma unroll
+        for (int h = lane; h < kH; h += 32) {
+          fetch_row(S, PS, buf ^ 1, h, r0 + ts + kH + h);
+          fetch_col(S, PS, c0, ts + kH + kW - 1 + h);
+        }
       }
 
       // ---- compute the tile: kH rows x kD diagonals per lane ----------------
@@ -603,9 +619,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
               cov[d] = fma(ru.y, cU[sl].x, cov[d]);
               hcs[d] = __double2hiint(cov[d] * (ri.x * cpk[sl]));  // rinv*cinv off the cov chain
             }
-            static_assert(kD == 8 || kD == 4, "fire test written for 4 or 8 diagonals per lane");
             int rmax;
-            if constexpr (kD == 8) {
+            if constexpr (kD == 12) {
+              const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
+              const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
+              const int m3 = __vimax3_s32(hcs[6], hcs[7], hcs[8]);
+              const int m4 = __vimax3_s32(hcs[9], hcs[10], hcs[11]);
+              rmax = __vimax3_s32(m1, m2, max(m3, m4));
+            } else if constexpr (kD == 16) {
+              const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
+              const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
+              const int m3 = __vimax3_s32(hcs[6], hcs[7], hcs[8]);
+              const int m4 = __vimax3_s32(hcs[9], hcs[10], hcs[11]);
+              const int m5 = __vimax3_s32(hcs[12], hcs[13], hcs[14]);
+              rmax = max(__vimax3_s32(m1, m2, m3), __vimax3_s32(m4, m5, hcs[15]));
+            } else if constexpr (kD == 8) {
               const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
               const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
               const int m3 = __vimax3_s32(hcs[6], hcs[7], m1);
@@ -695,9 +723,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       // ---- land the prefetch (warp-local) -------------------------------------
       if (t + 1 < nT) {
         cp_async_wait_all();
-        if (lane < kH) {
-          fix_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane, imask);
-          fix_col(S, PS, c0, ts + kH + kW - 1 + lane, imask);
+        if constexpr (kH <= 32) {
+          if (lane < kH) {
+            fix_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane, imask);
+            fix_col(S, PS, c0, ts + kH + kW - 1 + lane, imask);
+          }
+        } else {
+#pragma unroll
+          for (int h = lane; h < kH; h += 32) {
+            fix_row(S, PS, buf ^ 1, h, r0 + ts + kH + h, imask);
+            fix_col(S, PS, c0, ts + kH + kW - 1 + h, imask);
+          }
         }
       }
       __syncwarp();

@@ -24,7 +24,8 @@ r = subprocess.run(cmd, capture_output=True, text=True)
 if r.returncode:
     sys.stderr.write(r.stderr)
     sys.exit(1)
-for line in r.stderr.splitlines():
-    if "k_join" in line or ("registers" in line and "_Z6k_join" in line):
-        pass
+lines = r.stderr.splitlines()
+for i, line in enumerate(lines):
+    if "Function properties for _ZN5mpgpu6k_join" in line:
+        sys.stderr.write(name + ": " + " ".join(x.strip() for x in lines[i + 1:i + 3]) + "\n")
 print(out)
