@@ -388,21 +388,23 @@ __device__ __noinline__ SlowOut slow_path(const SlowIn in, unsigned live, int rt
     atomicAdd(&stats[1], (unsigned long long)__popc(rmask));
     atomicAdd(&stats[2], (unsigned long long)__popc(cmask));
   }
-  // columns: one RED per candidate, raise the shared and register thresholds
-  while (cmask) {
-    const int d = __ffs(cmask) - 1;
-    cmask &= cmask - 1;
-    const double c = pick(in.c, d);
-    const long long x = x0 + d;
-    const long long key = mk_key(c, i, imask);
-    red_min(&keyC[c0 + x], key);
-    const int th = lower_thr(__double2hiint(thr_filter(key, imask)));
+  // columns: one RED per candidate, raise the shared and register thresholds.
+  // Unrolled over the kD static slots (predicated per candidate): no dynamic
+  // register indexing, no jump table, no local memory.
+  if (cmask) {
 #pragma unroll
-    for (int q = 0; q < kD; ++q)
-      if (q == d && th > out.cthr[q]) out.cthr[q] = th;
-    const int a = ring_addr(x);
-    const double2 ci = S.colI[a];
-    if (th > __double2loint(ci.y)) S.colI[a].y = pack_col(ci.x, th);  // lanes of one warp: benign race
+    for (int d = 0; d < kD; ++d) {
+      if ((cmask >> d) & 1u) {
+        const long long x = x0 + d;
+        const long long key = mk_key(in.c[d], i, imask);
+        red_min(&keyC[c0 + x], key);
+        const int th = lower_thr(__double2hiint(thr_filter(key, imask)));
+        out.cthr[d] = th > out.cthr[d] ? th : out.cthr[d];
+        const int a = ring_addr(x);
+        const double2 ci = S.colI[a];
+        if (th > __double2loint(ci.y)) S.colI[a].y = pack_col(ci.x, th);  // lanes of one warp: benign race
+      }
+    }
   }
   // row: the lane's smallest key over its candidates (branch-free), then the warp's
   if (__any_sync(0xffffffffu, rmask != 0)) {
