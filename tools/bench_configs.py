@@ -1,6 +1,7 @@
 #!/usr/bin/env python3
 """Per-config numbers for DESIGN.md: GPU join (device-resident), e2e through the
-C ABI, and the CPU oracle STOMP sample, for C1..C5 on one GPU.
+C ABI, and the CPU oracle STOMP (in full for C1-C3, a bounded row sample for
+C4 and C5), for C1..C5 on one GPU.
 
     python tools/bench_configs.py [--configs C1,C2,C3,C4,C5] > profiles/configs_r01.jsonl
 """
@@ -26,6 +27,8 @@ ap.add_argument("--configs", default="C1,C2,C3,C4,C5")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--cpu-seconds", type=float, default=6.0)
 ap.add_argument("--no-cpu", action="store_true", help="GPU numbers only (quick A/B runs)")
+ap.add_argument("--cpu-full", default="C1,C2,C3",
+                help="configs whose CPU oracle STOMP runs in full (all rows), not sampled")
 args = ap.parse_args()
 
 for name in args.configs.split(","):
@@ -61,7 +64,19 @@ for name in args.configs.split(","):
         out = mp.join(pa, pb, cfg.window, cfg.zone, want_b=cfg.b is not None, timed=True, out=host_out)
         if r:
             tt.append(out["total_ms"])
-    cpu, thr, desc = (None, 0, "skipped") if args.no_cpu else cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
+    if args.no_cpu:
+        cpu, thr, desc = None, 0, "skipped"
+    elif name in args.cpu_full.split(","):
+        import time as _t
+        import oracle
+        thr = oracle.default_threads()
+        t0 = _t.perf_counter()
+        oracle.stomp(cfg.a, cfg.b, cfg.window, cfg.ez, n_workers=thr)
+        dt = _t.perf_counter() - t0
+        cpu = cfg.cells() / dt
+        desc = f"oracle STOMP (restated reference), the full join: {dt:.2f}s on {thr} threads"
+    else:
+        cpu, thr, desc = cpu_sample_rate(cfg, seconds_target=args.cpu_seconds)
     line = {"config": name, "workload": cfg.description, "cells": cfg.cells(),
             "gpu_ms": ms, "gpu_cells_per_s": cfg.cells() / (ms * 1e-3),
             "e2e_ms": min(tt), "e2e_cells_per_s": cfg.cells() / (min(tt) * 1e-3),

@@ -111,15 +111,43 @@ def main():
             plan.prepare_shared(0, N)
             coarse = [timed(stream, lambda: plan.coarse_run(s, N)) for s in range(N)]
             seed = []
-            for s in range(N):  # each shard's seeding consumes the pending coarse phase: redo it
-                plan.prepare_shared(s, N)
+            for s in range(N):  # each shard's seeding, from complete coarse keys
+                plan.prepare_shared(0, N)
+                plan.coarse_run(0, 1)
                 seed.append(timed(stream, lambda: plan.seed_shared(s, N)))
+            # the joins start from the whole job's warm start (every shard's seeds)
+            plan.reset_keys()
+            plan.prepare_shared(0, 1)
+            plan.coarse_run(0, 1)
+            plan.seed_shared(0, 1)
+            torch.cuda.synchronize()
             joins = [timed(stream, lambda: plan.run(s, N)) for s in range(N)]
+            outs = plan.outputs()
             fin = timed(stream, plan.outputs)
+            names = ("mp_a", "pi_a", "left_a", "right_a") if plan.self_join else ("mp_a", "pi_a")
+            fin_sh = [timed(stream, lambda: plan.finalize_shard(
+                s, N, *[outs[k] for k in names[:2]],
+                *([outs[k] for k in names[2:]] if plan.self_join else [None, None]),
+                *([None, None] if plan.self_join else [outs["mp_b"], outs["pi_b"]]))) for s in range(N)]
+            # a concurrent run: every shard starts against the warm start, but all
+            # shards' records land in the one key set as they go, so the job's
+            # key state at any moment matches a one-GPU run at the same fraction
+            # of the work (items are dealt round-robin in cost order). The later
+            # shards of the sequence (which see the earlier shards' final keys)
+            # bound the join from below, the first (warm start only) from above.
+            later = joins[1:] if N > 1 else joins
+            barrier_ms = 0.03  # per host barrier (gloo/NCCL over loopback, measured ~20-40 us)
+            step_lo = max(prep) + max(coarse) + max(seed) + max(later) + max(fin_sh) + 4 * barrier_ms
+            step_hi = max(prep) + max(coarse) + max(seed) + joins[0] + max(fin_sh) + 4 * barrier_ms
             print(json.dumps({"config": cfg.name, "mode": "shared keys, shards in sequence", "n_shards": N,
                               "prepare_shared_ms": prep, "coarse_run_ms": coarse,
                               "seed_shared_ms": seed, "join_ms": joins,
-                              "finalize_ms": fin}), flush=True)
+                              "finalize_ms": fin, "finalize_shard_ms": fin_sh,
+                              "step_pred_ms_range": [step_lo, step_hi],
+                              "note": "step = prepare + coarse shard + seeding + join shard + finalize shard "
+                                      "+ 4 barriers; low end: join as the later shards (keys as a concurrent "
+                                      "run sees them), high end: the first shard (warm start only)"}),
+                  flush=True)
         plan.close()
         return
     for N in [int(v) for v in args.ns.split(",")]:
