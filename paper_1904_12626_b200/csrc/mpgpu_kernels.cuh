@@ -759,7 +759,7 @@ struct DiagItem {
   int seg;    // rows [seg * rows, (seg + 1) * rows)
 };
 
-__global__ void __launch_bounds__(256) k_diag_join(const Series A, long long* __restrict__ keyR,
+__global__ void __launch_bounds__(256, 2) k_diag_join(const Series A, long long* __restrict__ keyR,
                                                    long long* __restrict__ keyC,
                                                    const long long* __restrict__ diags,
                                                    long long n_diags, const DiagItem* __restrict__ items,
@@ -785,37 +785,56 @@ __global__ void __launch_bounds__(256) k_diag_join(const Series A, long long* __
       const double* xj = A.x + r0 + k;
       for (int t = 0; t < m; ++t) cov = fma(xi[t] - mi, xj[t] - mj, cov);
     }
-    // the warp walks the longest lane's rows; shorter lanes idle at the end
+    // the warp walks the longest lane's rows; shorter lanes idle at the end.
+    // Rows go in batches of kDiagBatch: every load of a batch (the lane's
+    // column data, the broadcast row data, the keys) is issued before the
+    // batch's recurrence, so the dependent chain never waits on memory.
     long long rmax = r1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-    for (long long i = r0; i < rmax; ++i) {
-      const bool on = i < r1;
-      const long long j = i + (on ? k : 0);
-      const double2 ru = A.U[i];
-      const double ri = A.inv[i];
-      long long kr = kKeyNone;
-      if (on) {
-        if (i > r0) {
-          const double2 cu = A.U[j];
-          cov = fma(ru.x, cu.y, cov);
-          cov = fma(ru.y, cu.x, cov);
-        }
-        const double cj = A.inv[j];
-        const bool fi = ri == 0.0, fj = cj == 0.0;
-        const double c = (fi && fj) ? 1.0 : ((fi || fj) ? half_corr : cov * (ri * cj));
-        const long long kc = mk_key(c, i, imask);
-        if (kc < keyC[j]) red_min(&keyC[j], kc);
-        kr = mk_key(c, j, imask);
-      }
-      const long long cur = keyR[i];  // same address for every lane: one broadcast load
-      if (__any_sync(0xffffffffu, kr < cur)) {
+    constexpr int kDiagBatch = 4;
+    for (long long i0 = r0; i0 < rmax; i0 += kDiagBatch) {
+      double2 ru[kDiagBatch], cu[kDiagBatch];
+      double ri[kDiagBatch], cj[kDiagBatch];
+      long long kcur[kDiagBatch], rcur[kDiagBatch];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const long long v = __shfl_xor_sync(0xffffffffu, kr, o);
-          kr = v < kr ? v : kr;
+      for (int q = 0; q < kDiagBatch; ++q) {
+        const long long i = min(i0 + q, rmax - 1);  // rows past rmax repeat the last (unused)
+        const bool on = i0 + q < r1;
+        const long long j = on ? i + k : i;
+        ru[q] = A.U[i];
+        ri[q] = A.inv[i];
+        rcur[q] = keyR[i];
+        cu[q] = A.U[j];
+        cj[q] = A.inv[j];
+        kcur[q] = keyC[j];
+      }
+#pragma unroll
+      for (int q = 0; q < kDiagBatch; ++q) {
+        const long long i = i0 + q;
+        if (i >= rmax) break;  // warp-uniform
+        const bool on = i < r1;
+        long long kr = kKeyNone;
+        if (on) {
+          if (i > r0) {
+            cov = fma(ru[q].x, cu[q].y, cov);
+            cov = fma(ru[q].y, cu[q].x, cov);
+          }
+          const bool fi = ri[q] == 0.0, fj = cj[q] == 0.0;
+          const double c = (fi && fj) ? 1.0 : ((fi || fj) ? half_corr : cov * (ri[q] * cj[q]));
+          const long long kc = mk_key(c, i, imask);
+          if (kc < kcur[q]) red_min(&keyC[i + k], kc);
+          kr = mk_key(c, i + k, imask);
         }
-        if (lane == 0 && kr < cur) red_min(&keyR[i], kr);
+        const long long cur = rcur[q];
+        if (__any_sync(0xffffffffu, kr < cur)) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const long long v = __shfl_xor_sync(0xffffffffu, kr, o);
+            kr = v < kr ? v : kr;
+          }
+          if (lane == 0 && kr < cur) red_min(&keyR[i], kr);
+        }
       }
     }
   }

@@ -48,35 +48,43 @@ def emit(d):
 
 
 def anytime_scrimp():
-    """Anytime SCRIMP on C4 at 10% of the diagonals: the same k_join over a seeded band subset."""
+    """Anytime SCRIMP on C4 at 10% of the diagonals, both granularities: the band
+    fast path (the same k_join over a seeded band subset) and the reference's
+    exact per-diagonal order (k_diag_join, one diagonal per lane)."""
     c = datasets.c4()
     L = c.a.size - c.window + 1
-    s_size = (L - c.zone - 1) // 10
+    nd = L - c.zone - 1
+    s_size = nd // 10
     bands, coverage = mp.scrimp_bands(c.a.size, c.window, c.zone, s_size, seed=7)
-    ms = []
-    for r in range(3):
-        t0 = time.perf_counter()
-        prof = mp.scrimp(c.a, c.window, c.ez, s_size=s_size, seed=7)
-        ms.append((time.perf_counter() - t0) * 1e3)
-    # cells evaluated: sum over the chosen bands' diagonals of (L - k)
-    cells = 0
-    for b in bands:
-        k0 = c.zone + 1 + 256 * int(b)
-        k1 = min(k0 + 256, L)
-        cells += sum(L - k for k in range(k0, k1))
-    # CPU: the oracle's SCRIMP loop over a few of the same diagonals
+    diags_exact, cov_exact = mp.scrimp_diagonals(c.a.size, c.window, c.zone, s_size, seed=7)
+    # CPU: the oracle's SCRIMP loop over a few of the band diagonals
     diags = np.arange(c.zone + 1 + 256 * int(bands[0]), c.zone + 1 + 256 * int(bands[0]) + 64)
     t0 = time.perf_counter()
     oracle.scrimp_diagonals(c.a, c.window, diags, threads=THREADS)
     cpu_s = time.perf_counter() - t0
     cpu_cells = sum(L - int(k) for k in diags)
-    e2e = float(np.median(ms))
-    emit({"row": "8f.1 anytime SCRIMP", "workload": "C4, s_size = 10% of diagonals, seed 7",
-          "coverage": prof.coverage, "bands": int(bands.size), "cells": cells,
-          "e2e_ms": e2e, "e2e_cells_per_s": cells / (e2e * 1e-3),
-          "note": "e2e through mprof.scrimp (host buffers, includes stats, warm start, finalize)",
-          "cpu_cells_per_s": cpu_cells / cpu_s, "cpu_threads": THREADS,
-          "cpu_sample": f"oracle SCRIMP loop over {diags.size} diagonals"})
+    for gran in ("band", "diagonal"):
+        ms = []
+        for r in range(3):
+            t0 = time.perf_counter()
+            prof = mp.scrimp(c.a, c.window, c.ez, s_size=s_size, seed=7, granularity=gran)
+            ms.append((time.perf_counter() - t0) * 1e3)
+        if gran == "band":  # cells evaluated: the chosen bands' diagonals, (L - k) each
+            cells = 0
+            for b in bands:
+                k0 = c.zone + 1 + 256 * int(b)
+                cells += sum(L - k for k in range(k0, min(k0 + 256, L)))
+        else:
+            cells = int(np.sum(L - diags_exact))
+        e2e = float(np.median(ms))
+        emit({"row": "8f.1 anytime SCRIMP", "granularity": gran,
+              "workload": "C4, s_size = 10% of diagonals, seed 7",
+              "coverage": prof.coverage, "bands": int(bands.size) if gran == "band" else None,
+              "diagonals": int(diags_exact.size) if gran == "diagonal" else None, "cells": cells,
+              "e2e_ms": e2e, "e2e_cells_per_s": cells / (e2e * 1e-3),
+              "note": "e2e through mprof.scrimp (host buffers, includes stats, warm start, finalize)",
+              "cpu_cells_per_s": cpu_cells / cpu_s, "cpu_threads": THREADS,
+              "cpu_sample": f"oracle SCRIMP loop over {diags.size} diagonals"})
 
 
 def mass_batch():
