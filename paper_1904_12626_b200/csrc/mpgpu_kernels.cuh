@@ -36,6 +36,11 @@ constexpr int kMinBlocks = MPGPU_MINBLOCKS;  // CTAs per SM the register budget 
 #define MPGPU_BLOCK 8
 #endif
 constexpr int kBlock = MPGPU_BLOCK;          // row-steps per branch-free block (divides kD)
+// per-lane prefetch streams in k_join's tile loop (MPGPU_NO_LANE_STREAMS: the
+// round-1 index arithmetic, for A/B runs)
+#if !defined(MPGPU_NO_LANE_STREAMS) && !defined(MPGPU_LANE_STREAMS)
+#define MPGPU_LANE_STREAMS 1
+#endif
 constexpr int kWarps = MPGPU_WARPS;          // warps per CTA (independent workers)
 constexpr int kThreads = kWarps * 32;      // 256
 constexpr int kW = 32 * kD;                // diagonals per band = per warp item (256)
@@ -567,15 +572,45 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       cpk[d] = S.colI[a].y;
     }
 
+#ifdef MPGPU_LANE_STREAMS
+    // Per-lane prefetch streams, set up once per item: the row and column this
+    // lane fetches for tile t + 1 sit at fixed offsets from these pointers
+    // (+ t * kH), and its ring slot advances by kH modulo kRing, so a tile's
+    // prefetch and fix-up need no 64-bit index arithmetic or indexed
+    // parameter loads.
+    const long long rr = r0 + kH + lane, cc = c0 + kH + kW - 1 + lane;
+    const double2* const sRU = R.U + rr;
+    const double* const sRI = R.inv + rr;
+    const long long* const sRK = PS.keyR + rr;
+    const double2* const sCU = C.U + cc;
+    const double* const sCI = C.inv + cc;
+    const long long* const sCK = PS.keyC + cc;
+    const long long rlim = R.L - rr, clim = C.L - cc;  // keys exist while ts < lim
+    int px = (kH + kW - 1 + lane) % kRing;             // ring position of this lane's column
+#endif
     for (int t = 0; t < nT; ++t) {
       const int buf = t & 1;
       const long long ts = (long long)t * kH;
+#ifdef MPGPU_LANE_STREAMS
+      const int pa = (px % kD) * kNB + px / kD;  // ring slot of the prefetched column
+#endif
       // ---- prefetch tile t+1 (its ring slots held columns retired by now) ----
       if constexpr (kH <= 32) {
+#ifdef MPGPU_LANE_STREAMS
+        if (t + 1 < nT && lane < kH) {
+          cp_async16(&S.rowU[buf ^ 1][lane], sRU + ts);
+          cp_async8(&S.rowI[buf ^ 1][lane].x, sRI + ts);
+          if (ts < rlim) cp_async8(&S.rowI[buf ^ 1][lane].y, sRK + ts);
+          cp_async16(&S.colU[pa], sCU + ts);
+          cp_async8(&S.colI[pa].x, sCI + ts);
+          if (ts < clim) cp_async8(&S.colI[pa].y, sCK + ts);
+        }
+#else
         if (t + 1 < nT && lane < kH) {
           fetch_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane);
           fetch_col(S, PS, c0, ts + kH + kW - 1 + lane);
         }
+#endif
       } else if (t + 1 < nT) {
 #pragma unroll
         for (int h = lane; h < kH; h += 32) {
@@ -726,10 +761,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
       if (t + 1 < nT) {
         cp_async_wait_all();
         if constexpr (kH <= 32) {
+#ifdef MPGPU_LANE_STREAMS
+          if (lane < kH) {
+            const double2 vr = S.rowI[buf ^ 1][lane];
+            const double tr = (ts < rlim && vr.x != 0.0) ? thr_filter(__double_as_longlong(vr.y), imask) : 2.0;
+            S.rowI[buf ^ 1][lane].y = __hiloint2double(lower_thr(__double2hiint(tr)), 0);
+            const double2 vc = S.colI[pa];
+            const double tc = (ts < clim && vc.x != 0.0) ? thr_filter(__double_as_longlong(vc.y), imask) : 2.0;
+            S.colI[pa].y = pack_col(vc.x, lower_thr(__double2hiint(tc)));
+          }
+#else
           if (lane < kH) {
             fix_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane, imask);
             fix_col(S, PS, c0, ts + kH + kW - 1 + lane, imask);
           }
+#endif
         } else {
 #pragma unroll
           for (int h = lane; h < kH; h += 32) {
@@ -738,6 +784,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
           }
         }
       }
+#ifdef MPGPU_LANE_STREAMS
+      px += kH;
+      if (px >= kRing) px -= kRing;
+#endif
       __syncwarp();
     }
   }
