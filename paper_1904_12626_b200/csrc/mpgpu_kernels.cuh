@@ -997,9 +997,10 @@ __global__ void k_paa(const double* __restrict__ x, long long nc, int f, double*
 // start above the series (j0 < 0) or lie in the exclusion zone are skipped or
 // seeded where they enter, exactly as before.
 constexpr int kExpWarps = 4;
-constexpr int kExpGroups = 4;
-constexpr int kExpChunk = 128;
-constexpr int kExpSpan = 32 * kExpGroups;  // diagonals per pass
+constexpr int kExpGroups = 1;
+constexpr int kExpSpan = 32 * kExpGroups;  // diagonals per pass (one per lane)
+constexpr int kExpT = 8;                   // seed terms per lane per chunk
+constexpr int kExpChunk = 32 * kExpT;      // seed terms per chunk (256)
 
 constexpr int kExpWalk = 32;  // rows staged per walk chunk
 
@@ -1009,6 +1010,7 @@ struct ExpSmem {
       double a[kExpChunk];
       double y[kExpChunk + kExpSpan];
     } seed;
+    double red[32][kExpSpan + 1];  // per-lane partial seeds, padded rows (conflict-free)
     struct {  // walk: rows [qc, qc + kExpWalk), the columns they meet
       double2 rU[kExpWalk];
       double rI[kExpWalk];
@@ -1018,6 +1020,15 @@ struct ExpSmem {
   };
 };
 
+// One warp per coarse window I: the nd fine diagonals around its match share
+// one row window, so their seeds are nd sliding dot products of that window
+// against one column span. The m terms are split across the lanes (lane l
+// takes terms [8l, 8l + 8) of every 256-term chunk, with the 39 column values
+// they meet in registers), every lane accumulates all 32 diagonals of a pass,
+// and a transposed sum through shared memory leaves diagonal l's seed in lane
+// l: 8 x 32 FMAs per lane per chunk instead of 256 serial FMAs with half the
+// lanes idle. Then each lane walks its diagonal for f rows with the join's
+// recurrence, RED.MINing into the keys (one warp-min RED per row).
 __global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
     const Pass PS, const long long* __restrict__ ckey, long long I0, long long I1, long long cimask,
     bool key_is_col, int f, int span, long long zone, bool self, int m, long long imask) {
@@ -1038,29 +1049,46 @@ __global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
   if (i0 >= R.L) return;
   const double mi = R.mu[i0];
   for (int d0 = 0; d0 < nd; d0 += kExpSpan) {
-    // seeds of diagonals d0 .. d0 + kExpSpan - 1 at row i0 (columns jbase + d)
-    double acc[kExpGroups], asum = 0.0;
-    const int ng = min(kExpGroups, (nd - d0 + 31) / 32);  // warp-uniform
+    constexpr int ng = 1;
+    // seeds of diagonals d0 .. d0 + 31 at row i0 (columns jbase + d0 + d)
+    double part[kExpSpan];
 #pragma unroll
-    for (int g = 0; g < kExpGroups; ++g) acc[g] = 0.0;
+    for (int d = 0; d < kExpSpan; ++d) part[d] = 0.0;
+    double asum_l = 0.0;
     for (int t0 = 0; t0 < m; t0 += kExpChunk) {
       const int tc = min(kExpChunk, m - t0);
-      for (int q = lane; q < tc; q += 32) S.seed.a[q] = R.x[i0 + t0 + q] - mi;
-      for (int q = lane; q < tc + 32 * ng; q += 32) {
+      for (int q = lane; q < kExpChunk; q += 32) S.seed.a[q] = q < tc ? R.x[i0 + t0 + q] - mi : 0.0;
+      for (int q = lane; q < kExpChunk + kExpSpan; q += 32) {
         const long long gidx = jbase + d0 + t0 + q;
-        S.seed.y[q] = (gidx >= 0 && gidx < C.n) ? C.x[gidx] : 0.0;
+        S.seed.y[q] = (q < tc + kExpSpan && gidx >= 0 && gidx < C.n) ? C.x[gidx] : 0.0;
       }
       __syncwarp();
-      for (int t = 0; t < tc; ++t) {
-        const double at = S.seed.a[t];
-        asum += at;
-        acc[0] = fma(at, S.seed.y[lane + t], acc[0]);
+      double av[kExpT], yv[kExpT + kExpSpan - 1];
 #pragma unroll
-        for (int g = 1; g < kExpGroups; ++g)
-          if (g < ng) acc[g] = fma(at, S.seed.y[lane + 32 * g + t], acc[g]);
+      for (int tt = 0; tt < kExpT; ++tt) {
+        av[tt] = S.seed.a[lane * kExpT + tt];
+        asum_l += av[tt];
       }
+#pragma unroll
+      for (int u = 0; u < kExpT + kExpSpan - 1; ++u) yv[u] = S.seed.y[lane * kExpT + u];
+#pragma unroll
+      for (int tt = 0; tt < kExpT; ++tt)
+#pragma unroll
+        for (int d = 0; d < kExpSpan; ++d) part[d] = fma(av[tt], yv[tt + d], part[d]);
       __syncwarp();
     }
+    // transposed sum: lane d collects every lane's partial of diagonal d
+#pragma unroll
+    for (int d = 0; d < kExpSpan; ++d) S.red[lane][d] = part[d];
+    __syncwarp();
+    double acc[kExpGroups];
+    acc[0] = 0.0;
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) acc[0] += S.red[l][lane];
+    double asum = asum_l;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) asum += __shfl_xor_sync(0xffffffffu, asum, o);
+    __syncwarp();
     // per lane and group: the diagonal's first row q0 and end qn (q0 >= qn: skip)
     long long q0s[kExpGroups], qns[kExpGroups];
 #pragma unroll
