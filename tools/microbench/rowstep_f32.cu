@@ -17,17 +17,25 @@ struct __align__(16) WS {
   double2 rowI[kH + 1];
 };
 
-__device__ __forceinline__ int f32bits_of_hi(int h, bool clamp) {
+__device__ __forceinline__ int f32bits_of_hi(int h, int clamp) {
   // (h << 3) - (896 << 23): exponent rebias 1023 -> 127, 20 mantissa bits.
-  // clamp: max(h, hi(2^-121)) first, so negative / tiny covariances map to a
-  // tiny positive float instead of wrapping.
-  if (clamp) h = max(h, (1023 - 121) << 20);
+  // clamp 1: max(h, hi(2^-121)) first, so negative / tiny covariances map to a
+  // tiny positive float instead of wrapping; clamp 2: also min(h, hi(2^128)),
+  // so huge covariances map to +inf (a conservative fire) instead of wrapping.
+  if (clamp >= 1) h = max(h, (1023 - 121) << 20);
+  if (clamp >= 2) h = min(h, (1023 + 128) << 20);
   return (h << 3) - (896 << 23);
 }
 
 // MODE 0: fp64 filter (production). 1: fp32 filter with the clamp. 2: fp32, no clamp.
+#ifndef RS_WARPS
+#define RS_WARPS 8
+#endif
+#ifndef RS_MINB
+#define RS_MINB 2
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) k(double* out, int tiles) {
+__global__ void __launch_bounds__(RS_WARPS * 32, RS_MINB) k(double* out, int tiles) {
   extern __shared__ __align__(16) unsigned char sm[];
   WS& S = reinterpret_cast<WS*>(sm)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -96,7 +104,7 @@ __global__ void __launch_bounds__(256, 2) k(double* out, int tiles) {
             const int sl = (s + d) % kD;
             cov[d] = fma(ru.x, cU[sl].y, cov[d]);
             cov[d] = fma(ru.y, cU[sl].x, cov[d]);
-            cf[d] = __int_as_float(f32bits_of_hi(__double2hiint(cov[d]), MODE == 1));
+            cf[d] = __int_as_float(f32bits_of_hi(__double2hiint(cov[d]), MODE == 1 ? 1 : (MODE == 3 ? 2 : 0)));
           }
 #pragma unroll
           for (int d = 0; d < kD; d += 2) {
@@ -131,27 +139,27 @@ __global__ void __launch_bounds__(256, 2) k(double* out, int tiles) {
 template <int MODE>
 void run(const char* name, int nsm, double* dout) {
   const int tiles = 600;
-  const size_t smem = 8 * sizeof(WS);
+  const size_t smem = RS_WARPS * sizeof(WS);
   cudaFuncSetAttribute(k<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int blocks = nsm * 2 * 4;
-  k<MODE><<<blocks, 256, smem>>>(dout, 2);
+  const int blocks = nsm * RS_MINB * 4;
+  k<MODE><<<blocks, RS_WARPS * 32, smem>>>(dout, 2);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float best = 1e30f;
   for (int r = 0; r < 3; ++r) {
     cudaEventRecord(e0);
-    k<MODE><<<blocks, 256, smem>>>(dout, tiles);
+    k<MODE><<<blocks, RS_WARPS * 32, smem>>>(dout, tiles);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     best = ms < best ? ms : best;
   }
-  const double cells = (double)blocks * 256 * tiles * kH * kD;
-  const double rowsteps_per_smsp = (double)blocks * 8 * tiles * kH / (nsm * 4);
-  printf("{\"variant\": \"%s\", \"cells_per_s\": %.3e, \"cycles_per_rowstep_at_1965\": %.1f, \"err\": \"%s\"}\n",
-         name, cells / (best * 1e-3), best * 1e-3 * 1.965e9 / rowsteps_per_smsp,
+  const double cells = (double)blocks * RS_WARPS * 32 * tiles * kH * kD;
+  const double rowsteps_per_smsp = (double)blocks * RS_WARPS * tiles * kH / (nsm * 4);
+  printf("{\"warps\": %d, \"minb\": %d, \"variant\": \"%s\", \"cells_per_s\": %.3e, \"cycles_per_rowstep_at_1965\": %.1f, \"err\": \"%s\"}\n",
+         RS_WARPS, RS_MINB, name, cells / (best * 1e-3), best * 1e-3 * 1.965e9 / rowsteps_per_smsp,
          cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -164,5 +172,6 @@ int main() {
   run<0>("fp64 filter (2 DMUL/cell)", nsm, dout);
   run<1>("fp32 filter, IMNMX clamp + LEA + FMUL2(cov*rinv) + FMUL(*cinv)", nsm, dout);
   run<2>("fp32 filter, LEA + FMUL2 + FMUL, no clamp", nsm, dout);
+  run<3>("fp32 filter, two-sided clamp (IMNMX x2) + LEA + FMUL2 + FMUL", nsm, dout);
   return 0;
 }
