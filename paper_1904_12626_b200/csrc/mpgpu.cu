@@ -525,8 +525,10 @@ mpgpu_plan* mpgpu_plan_create(const double* d_a, int64_t n_a, const double* d_b,
     return nullptr;
   }
   p->imask = (1LL << p->index_bits) - 1;
-  if (cudaMalloc(&p->key0, sizeof(long long) * p->A.L) != cudaSuccess ||
-      cudaMalloc(&p->key1, sizeof(long long) * Lb) != cudaSuccess ||
+  // keys carry kPad entries of padding like the statistics (kernels may read,
+  // never use, a few entries past the end)
+  if (cudaMalloc(&p->key0, sizeof(long long) * (p->A.L + kPad)) != cudaSuccess ||
+      cudaMalloc(&p->key1, sizeof(long long) * (Lb + kPad)) != cudaSuccess ||
       cudaMalloc(&p->d_counter, sizeof(int)) != cudaSuccess) {
     fail(MPGPU_ENOMEM, "key allocation failed");
     mpgpu_plan_destroy(p.release());
@@ -937,8 +939,8 @@ KeyLayout key_layout(const mpgpu_plan* p) {
   KeyLayout k{};
   const long long Lb = p->self ? p->A.L : p->B.L;
   k.off[0] = 0;
-  k.off[1] = up(8 * p->A.L);
-  long long end = k.off[1] + up(8 * Lb);
+  k.off[1] = up(8 * (p->A.L + kPad));  // padded like the plan's own key arrays
+  long long end = k.off[1] + up(8 * (Lb + kPad));
   k.coarse = p->coarse_f > 0 && !p->subset;
   if (k.coarse) {
     const long long f = p->coarse_f, mc = p->m / f;

@@ -838,44 +838,57 @@ __global__ void __launch_bounds__(256, 2) k_diag_join(const Series A, long long*
     // the warp walks the longest lane's rows; shorter lanes idle at the end.
     // Rows go in batches of kDiagBatch: every load of a batch (the lane's
     // column data, the broadcast row data, the keys) is issued before the
-    // batch's recurrence, so the dependent chain never waits on memory.
+    // batch's recurrence, so the dependent chain never waits on memory. All
+    // addressing is 32-bit offsets from per-item base pointers, and a cell's
+    // two keys share one score computation.
     long long rmax = r1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rmax = max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    const int nrows = (int)(rmax - r0);       // warp-uniform
+    const int mine = (int)(r1 - r0);          // this lane's rows (0 when it has no diagonal)
+    const long long jb = r0 + (k >= 0 ? k : 0);
+    // per-lane streams, bumped by a batch each step: the loads use immediate
+    // offsets. Reads run up to kDiagBatch - 1 entries past a stream's end into
+    // the padding every statistics and key array carries (kPad entries).
+    const double2* pRU = A.U + r0;
+    const double* pRI = A.inv + r0;
+    long long* pRK = keyR + r0;
+    const double2* pCU = A.U + jb;
+    const double* pCI = A.inv + jb;
+    long long* pCK = keyC + jb;
     constexpr int kDiagBatch = 4;
-    for (long long i0 = r0; i0 < rmax; i0 += kDiagBatch) {
+    for (int q0 = 0; q0 < nrows; q0 += kDiagBatch) {
       double2 ru[kDiagBatch], cu[kDiagBatch];
       double ri[kDiagBatch], cj[kDiagBatch];
       long long kcur[kDiagBatch], rcur[kDiagBatch];
 #pragma unroll
       for (int q = 0; q < kDiagBatch; ++q) {
-        const long long i = min(i0 + q, rmax - 1);  // rows past rmax repeat the last (unused)
-        const bool on = i0 + q < r1;
-        const long long j = on ? i + k : i;
-        ru[q] = A.U[i];
-        ri[q] = A.inv[i];
-        rcur[q] = keyR[i];
-        cu[q] = A.U[j];
-        cj[q] = A.inv[j];
-        kcur[q] = keyC[j];
+        ru[q] = pRU[q];
+        ri[q] = pRI[q];
+        rcur[q] = pRK[q];
+        cu[q] = pCU[q];
+        cj[q] = pCI[q];
+        kcur[q] = pCK[q];
       }
 #pragma unroll
       for (int q = 0; q < kDiagBatch; ++q) {
-        const long long i = i0 + q;
-        if (i >= rmax) break;  // warp-uniform
-        const bool on = i < r1;
-        long long kr = kKeyNone;
-        if (on) {
-          if (i > r0) {
-            cov = fma(ru[q].x, cu[q].y, cov);
-            cov = fma(ru[q].y, cu[q].x, cov);
-          }
-          const bool fi = ri[q] == 0.0, fj = cj[q] == 0.0;
-          const double c = (fi && fj) ? 1.0 : ((fi || fj) ? half_corr : cov * (ri[q] * cj[q]));
-          const long long kc = mk_key(c, i, imask);
-          if (kc < kcur[q]) red_min(&keyC[i + k], kc);
-          kr = mk_key(c, i + k, imask);
+        const int qq = q0 + q;
+        if (qq >= nrows) break;  // warp-uniform
+        const bool on = qq < mine;
+        if (on && qq > 0) {
+          cov = fma(ru[q].x, cu[q].y, cov);
+          cov = fma(ru[q].y, cu[q].x, cov);
         }
+        // score = 1 - corr, clamped at 0; flat windows take the convention
+        // (both flat: 0, one flat: 1/2)
+        const double nn = ri[q] * cj[q];
+        double sc = 1.0 - cov * nn;
+        sc = sc > 0.0 ? sc : 0.0;
+        if (nn == 0.0) sc = (ri[q] == 0.0 && cj[q] == 0.0) ? 0.0 : 0.5;
+        const long long sb = __double_as_longlong(sc) & ~imask;
+        const long long kc = sb | (r0 + qq);          // column key: neighbour i
+        long long kr = on ? (sb | (jb + qq)) : kKeyNone;  // row key: neighbour j
+        if (on && kc < kcur[q]) red_min(pCK + q, kc);
         const long long cur = rcur[q];
         if (__any_sync(0xffffffffu, kr < cur)) {
 #pragma unroll
@@ -883,9 +896,15 @@ __global__ void __launch_bounds__(256, 2) k_diag_join(const Series A, long long*
             const long long v = __shfl_xor_sync(0xffffffffu, kr, o);
             kr = v < kr ? v : kr;
           }
-          if (lane == 0 && kr < cur) red_min(&keyR[i], kr);
+          if (lane == 0 && kr < cur) red_min(pRK + q, kr);
         }
       }
+      pRU += kDiagBatch;
+      pRI += kDiagBatch;
+      pRK += kDiagBatch;
+      pCU += kDiagBatch;
+      pCI += kDiagBatch;
+      pCK += kDiagBatch;
     }
   }
 }

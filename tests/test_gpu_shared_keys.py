@@ -33,3 +33,29 @@ def test_shared_keys_join_matches_single_process(nproc, n, m, kind):
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
+
+
+@pytest.mark.gpu
+def test_key_region_owner_table():
+    """The striped region's chunk owners (mpgpu_plan_key_region_owners): every
+    chunk has an owner, every rank owns a chunk when there are enough, the
+    busiest rank's modelled share of the key reads is at least 1/N and, at
+    C5-like sizes, close to it."""
+    import numpy as np
+    import torch
+    import paper_1904_12626_b200 as mp
+    x = torch.from_numpy(np.cumsum(np.random.default_rng(3).standard_normal(1 << 21))).cuda()
+    plan = mp.Plan(x, None, 128, 64)
+    gran = int(mp.lib().mpgpu_stripes_granularity(plan.device))
+    assert gran >= 1 << 21
+    nbytes = plan.key_region_bytes()
+    for n in (1, 2, 3, 8):
+        owners, share = plan.key_region_owners(gran, n)
+        assert len(owners) == -(-nbytes // gran)
+        assert all(0 <= o < n for o in owners)
+        if len(owners) >= n:
+            assert set(owners) == set(range(n))
+        assert 1.0 / n - 1e-9 <= share <= 1.0
+    owners, share = plan.key_region_owners(gran, 2)
+    assert share < 0.55  # 2^21 windows: 33 chunks balance to ~1/2
+    plan.close()
