@@ -5,7 +5,8 @@ The profile must be bit-identical to a one-process join: cells never change
 arithmetic with sharding, and the shared keys are the exact MIN of every
 rank's candidates. n = 2^19 makes the warm start's rows per thread > 1 on one
 rank, where an earlier build sized them from the shard's share (the seed
-points then moved with the world size)."""
+points then moved with the world size). Eight ranks at n = 2^17 have fewer
+2 MB chunks than ranks: most ranks own no chunk and map the others' only."""
 import os
 import socket
 import subprocess
@@ -25,7 +26,7 @@ def _free_port():
 @pytest.mark.gpu
 @pytest.mark.parametrize("nproc,n,m,kind", [(2, 1 << 16, 128, "self"), (3, 1 << 14, 64, "self"),
                                             (2, 1 << 14, 100, "ab"), (2, 1 << 19, 128, "self"),
-                                            (3, 1 << 18, 200, "ab")])
+                                            (3, 1 << 18, 200, "ab"), (8, 1 << 17, 128, "self")])
 def test_shared_keys_join_matches_single_process(nproc, n, m, kind):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
