@@ -946,8 +946,8 @@ KeyLayout key_layout(const mpgpu_plan* p) {
     const long long f = p->coarse_f, mc = p->m / f;
     const long long Lca = p->A.n / f - mc + 1, Lcb = p->self ? Lca : p->B.n / f - mc + 1;
     k.off[2] = end;
-    k.off[3] = end + up(8 * Lca);
-    end = k.off[3] + up(8 * Lcb);
+    k.off[3] = end + up(8 * (Lca + kPad));
+    end = k.off[3] + up(8 * (Lcb + kPad));
   }
   k.bytes = end;
   return k;
