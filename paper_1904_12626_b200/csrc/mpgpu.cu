@@ -134,6 +134,12 @@ struct mpgpu_plan {
   bool subset = false;
   long long* d_init_diags = nullptr;  // anytime warm start: diagonals inside the chosen bands
   int n_init_diags = 0;
+  // anytime band subsets: the chosen bands as a bitmask (the coarse exploit
+  // seeds only their diagonals) and the coarse diagonals they map to (the
+  // coarse warm start joins only those)
+  unsigned* d_band_mask = nullptr;
+  std::vector<long long> coarse_diags;
+  bool coarse_diags_dirty = false;
   // anytime (SCRIMP) over an explicit diagonal set: k_diag_join instead of k_join
   bool diag_mode = false;
   long long* d_diags = nullptr;
@@ -378,6 +384,8 @@ mpgpu_status coarse_finish(mpgpu_plan* p, int shard = 0, int n_shards = 1) {
   static const int span_env = getenv("MPGPU_COARSE_SPAN") ? atoi(getenv("MPGPU_COARSE_SPAN")) : 0;
   const int dspan = span_env > 0 ? span_env : std::max(1, f / 2);
   const int nd = 2 * dspan + 1;
+  // anytime band subsets: seed only diagonals of the chosen bands
+  const unsigned* band_mask = (p->subset && !p->diag_mode) ? p->d_band_mask : nullptr;
   // this shard's contiguous share of the coarse windows (all of them for one shard)
   const long long r0 = Lr * shard / n_shards, r1 = Lr * (shard + 1) / n_shards;
   const long long c0 = Lc * shard / n_shards, c1 = Lc * (shard + 1) / n_shards;
@@ -385,11 +393,11 @@ mpgpu_status coarse_finish(mpgpu_plan* p, int shard = 0, int n_shards = 1) {
   if (r1 > r0)
     k_coarse_exploit<<<(unsigned)((r1 - r0 + kExpWarps - 1) / kExpWarps), kExpWarps * 32, 0,
                        p->stream>>>(P.pass[0], key_row(c), r0, r1, c->imask, false, f, dspan,
-                                    p->zone, p->self, (int)p->m, p->imask);
+                                    p->zone, p->self, (int)p->m, p->imask, band_mask);
   if (c1 > c0)
     k_coarse_exploit<<<(unsigned)((c1 - c0 + kExpWarps - 1) / kExpWarps), kExpWarps * 32, 0,
                        p->stream>>>(P.pass[0], key_col(c), c0, c1, c->imask, true, f, dspan,
-                                    p->zone, p->self, (int)p->m, p->imask);
+                                    p->zone, p->self, (int)p->m, p->imask, band_mask);
   p->launches += 2;
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
@@ -430,6 +438,10 @@ void launch_init(mpgpu_plan* p, int shard, int n_shards) {
 std::once_flag g_attr_once;
 int g_ctas_per_sm = 0;
 
+}  // namespace
+
+namespace {
+mpgpu_status plan_select_diagonals(mpgpu_plan* p, const std::vector<long long>& diags);
 }  // namespace
 
 namespace mpgpu_internal {
@@ -574,6 +586,7 @@ void mpgpu_plan_destroy(mpgpu_plan* p) {
   cudaFree(p->d_init_diags);
   cudaFree(p->d_diags);
   cudaFree(p->d_ditems);
+  cudaFree(p->d_band_mask);
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
   delete p;
 }
@@ -737,6 +750,21 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
     k_init_keys<<<grid, kInitWarps * 32, 0, p->stream>>>(ps, p->zone + 1, ps.C.L, (int)p->m,
                                                          p->imask, p->d_init_diags, 0, 1, n_init);
     p->launches += 1;
+  }
+  if (p->subset && !p->diag_mode && p->coarse_f > 0 && !p->coarse_diags.empty()) {
+    // anytime band subset: the coarse warm start restricted to the coarse
+    // diagonals the chosen bands map to (a diagonal-subset join of the PAA
+    // series), its exploit seeding only the chosen bands' diagonals
+    bool ok = ensure_coarse(p) == MPGPU_OK;
+    if (ok && p->coarse_diags_dirty) {
+      ok = plan_select_diagonals(p->coarse, p->coarse_diags) == MPGPU_OK;
+      p->coarse_diags_dirty = !ok;
+    }
+    if (ok && coarse_begin(p, 0, 1) == MPGPU_OK) {
+      p->coarse_pending = true;
+    } else {
+      cudaGetLastError();
+    }
   }
   if (npass > 0 && p->coarse_f > 0) {
     // the coarse phase only tightens the filter: if it cannot run (e.g. the
@@ -1048,6 +1076,8 @@ mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int
     p->subset = false;
     p->diag_mode = false;
     p->bands.clear();
+    p->coarse_diags.clear();
+    if (p->coarse && p->coarse->subset) mpgpu_plan_select_bands(p->coarse, nullptr, -1);
     return MPGPU_OK;
   }
   p->diag_mode = false;
@@ -1086,6 +1116,33 @@ mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int
     MPG_CUDA(cudaMemcpy(p->d_init_diags, wd.data(), sizeof(long long) * wd.size(),
                         cudaMemcpyHostToDevice));
     p->n_init_diags = (int)wd.size();
+  }
+  // band bitmask for the coarse exploit, and the coarse diagonals the bands
+  // map to (fine diagonal k ~ coarse diagonal k / f, one either side)
+  {
+    const long long nbt = std::max<long long>(1, mpgpu_plan_num_bands(p));
+    std::vector<unsigned> mask((size_t)((nbt + 31) / 32), 0u);
+    for (long long k0 : kb) {
+      const long long b = (k0 - klo) / kW;
+      mask[(size_t)(b >> 5)] |= 1u << (b & 31);
+    }
+    cudaFree(p->d_band_mask);
+    p->d_band_mask = nullptr;
+    MPG_CUDA(cudaMalloc(&p->d_band_mask, sizeof(unsigned) * mask.size()));
+    MPG_CUDA(cudaMemcpy(p->d_band_mask, mask.data(), sizeof(unsigned) * mask.size(),
+                        cudaMemcpyHostToDevice));
+    p->coarse_diags.clear();
+    if (p->coarse_f > 0) {
+      const long long f = p->coarse_f, mc = p->m / f;
+      const long long Lc = p->A.n / f - mc + 1, zc = (p->zone + f - 1) / f;
+      for (long long k0 : kb) {
+        const long long lo = std::max(zc + 1, k0 / f - 1);
+        const long long hi = std::min(Lc - 1, (k0 + kW - 1) / f + 1);
+        for (long long K = lo; K <= hi; ++K)
+          if (p->coarse_diags.empty() || p->coarse_diags.back() < K) p->coarse_diags.push_back(K);
+      }
+    }
+    p->coarse_diags_dirty = true;
   }
   p->bands.swap(kb);
   p->subset = true;

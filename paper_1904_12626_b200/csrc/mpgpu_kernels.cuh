@@ -1050,7 +1050,8 @@ struct ExpSmem {
 // recurrence, RED.MINing into the keys (one warp-min RED per row).
 __global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
     const Pass PS, const long long* __restrict__ ckey, long long I0, long long I1, long long cimask,
-    bool key_is_col, int f, int span, long long zone, bool self, int m, long long imask) {
+    bool key_is_col, int f, int span, long long zone, bool self, int m, long long imask,
+    const unsigned* __restrict__ band_mask) {
   __shared__ ExpSmem sm[kExpWarps];
   ExpSmem& S = sm[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1118,6 +1119,10 @@ __global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
       qn = min(qn, R.L - i0);
       qn = min(qn, C.L - j0);
       if (d >= nd || g >= ng || (self && j0 - i0 <= zone)) q0 = qn = 0;  // none / in the zone
+      if (band_mask && q0 < qn) {  // anytime band subset: only the chosen bands' diagonals
+        const long long b = (j0 - i0 - zone - 1) / kW;
+        if (!((band_mask[b >> 5] >> (b & 31)) & 1u)) q0 = qn = 0;
+      }
       q0s[g] = q0;
       qns[g] = qn;
       if (q0 >= qn) continue;
