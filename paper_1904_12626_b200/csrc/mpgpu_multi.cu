@@ -34,7 +34,10 @@ namespace {
 
 using mpgpu_internal::set_error;
 
-constexpr int kMWarps = 8;                      // warps per CTA
+#ifndef MPGPU_MWARPS
+#define MPGPU_MWARPS 8
+#endif
+constexpr int kMWarps = MPGPU_MWARPS;           // warps per CTA
 constexpr long long kNoKey = 0x7fffffffffffffffLL;
 constexpr double kRawSnap = 1e-12;              // OR_RAW_SNAP, distance.hpp:54-57
 constexpr int kMaxMDims = 32;                   // mSTOMP admissible dims
