@@ -287,6 +287,54 @@ def main():
             flush_l2(l2)
         step(mk())
     torch.cuda.synchronize()
+    # N > 1: before anything is timed, rank 0 joins the whole job alone and the
+    # multi-rank profile must equal it bit for bit (the shards' cells have the
+    # same arithmetic and the keys are an exact MIN). The striped-key path has
+    # only ever run with several ranks on one GPU in this repo's tests, so a
+    # mismatch on real peers falls back, on every rank, to separate keys plus
+    # the NCCL MIN merge, and the line says so.
+    check = None
+    if world > 1:
+        forced = [os.environ.get("MPGPU_BENCH_FORCE_MISMATCH") == "1"]  # tests: exercise the fallback
+
+        def multi_rank_matches():
+            ok = True
+            if rank == 0:
+                with torch.cuda.stream(stream):
+                    ref_plan = mp.Plan(a, b, cfg.window, cfg.zone, stream=stream)
+                    ref_plan.prepare()
+                    ref_plan.run(0, 1)
+                    ref = ref_plan.outputs()
+                stream.synchronize()
+                ok = outs is not None and all(torch.equal(outs[k], ref[k]) for k in ref)
+                ref_plan.close()
+            if forced[0]:
+                ok, forced[0] = False, False
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                                device=dev if dist.get_backend() == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            return int(flag.item()) == 1
+
+        if cells_total > 1.5e12:
+            check = "skipped (a one-rank join of this size takes too long)"
+        else:
+            if args.warmup == 0:
+                step(mk())
+                torch.cuda.synchronize()
+            if multi_rank_matches():
+                check = "bit-identical to rank 0's one-rank join"
+            elif shared:
+                shared.close()
+                dist.barrier()
+                shared = None
+                os.environ["MPGPU_SHARED_KEYS"] = "0"  # the e2e leg follows suit
+                for _ in range(max(1, args.warmup)):
+                    step(mk())
+                torch.cuda.synchronize()
+                check = ("striped keys MISMATCHED the one-rank join; fell back to the NCCL MIN merge, "
+                         + ("which matches bit for bit" if multi_rank_matches() else "which MISMATCHES too"))
+            else:
+                check = "MISMATCH against rank 0's one-rank join"
     launches_per_step = plan.launches() + (0 if rank else 0)
 
     evs = []
@@ -360,6 +408,7 @@ def main():
                          "cells_per_launch": my_cells,
                          "peak_source": "measured fp64 microbench (profiles/fp64_peak_r01.jsonl), burst 1965 MHz"},
             "clocks": csum,
+            "multi_gpu_check": check,
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,

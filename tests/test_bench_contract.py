@@ -58,6 +58,31 @@ def test_bench_two_ranks_gloo_on_one_gpu():
     assert len(lines) == 1, r.stdout
     d = lines[0]
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["gpu_launches"] > 0
+    # the run-time check of the multi-rank profile against rank 0's one-rank join
+    assert d["multi_gpu_check"].startswith("bit-identical"), d["multi_gpu_check"]
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     # each rank evaluates about half of the cells
     assert 0.4 < d["roofline"]["cells_per_launch"] / d["config"]["cells_per_step"] < 0.6
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_separate_keys_check():
+    r = _torchrun(2, ["--gpus", "2", "--steps", "1", "--warmup", "1", "--config", "C1",
+                      "--no-cpu-baseline", "--no-e2e"],
+                  env_extra={"MPGPU_DIST_BACKEND": "gloo", "MPGPU_SHARED_KEYS": "0"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _json_lines(r.stdout)[0]
+    assert "NCCL MIN merge" in d["parallelism"]
+    assert d["multi_gpu_check"].startswith("bit-identical"), d["multi_gpu_check"]
+
+
+@pytest.mark.gpu
+def test_bench_falls_back_when_the_shared_key_profile_mismatches():
+    r = _torchrun(2, ["--gpus", "2", "--steps", "1", "--warmup", "1", "--config", "C1",
+                      "--no-cpu-baseline"],
+                  env_extra={"MPGPU_DIST_BACKEND": "gloo", "MPGPU_BENCH_FORCE_MISMATCH": "1"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = _json_lines(r.stdout)[0]
+    assert "NCCL MIN merge" in d["parallelism"]
+    assert "fell back" in d["multi_gpu_check"] and "matches bit for bit" in d["multi_gpu_check"]
+    assert "NCCL" in d["e2e"]["api"] and d["e2e"]["value"] > 0
