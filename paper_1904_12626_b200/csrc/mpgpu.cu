@@ -140,7 +140,12 @@ struct mpgpu_plan {
   unsigned* d_band_mask = nullptr;
   std::vector<long long> coarse_diags;
   bool coarse_diags_dirty = false;
-  // anytime (SCRIMP) over an explicit diagonal set: k_diag_join instead of k_join
+  // anytime (SCRIMP) over an explicit diagonal set: k_diag_join instead of k_join,
+  // or, for dense sets, k_join_masked over the bands that hold a chosen diagonal
+  // (mask_mode: subset is set too, bands lists those bands)
+  bool mask_mode = false;
+  unsigned char* d_dmasks = nullptr;  // per band and lane: the lane's chosen diagonals
+  uint32_t* d_diag_bits = nullptr;    // bit k: diagonal k is chosen
   bool diag_mode = false;
   long long* d_diags = nullptr;
   long long n_diags = 0;
@@ -385,7 +390,9 @@ mpgpu_status coarse_finish(mpgpu_plan* p, int shard = 0, int n_shards = 1) {
   const int dspan = span_env > 0 ? span_env : std::max(1, f / 2);
   const int nd = 2 * dspan + 1;
   // anytime band subsets: seed only diagonals of the chosen bands
-  const unsigned* band_mask = (p->subset && !p->diag_mode) ? p->d_band_mask : nullptr;
+  const unsigned* band_mask = (p->subset && !p->diag_mode && !p->mask_mode) ? p->d_band_mask : nullptr;
+  // masked bands (dense diagonal subsets): seed only the chosen diagonals
+  const unsigned* diag_bits = p->mask_mode ? p->d_diag_bits : nullptr;
   // this shard's contiguous share of the coarse windows (all of them for one shard)
   const long long r0 = Lr * shard / n_shards, r1 = Lr * (shard + 1) / n_shards;
   const long long c0 = Lc * shard / n_shards, c1 = Lc * (shard + 1) / n_shards;
@@ -393,11 +400,11 @@ mpgpu_status coarse_finish(mpgpu_plan* p, int shard = 0, int n_shards = 1) {
   if (r1 > r0)
     k_coarse_exploit<<<(unsigned)((r1 - r0 + kExpWarps - 1) / kExpWarps), kExpWarps * 32, 0,
                        p->stream>>>(P.pass[0], key_row(c), r0, r1, c->imask, false, f, dspan,
-                                    p->zone, p->self, (int)p->m, p->imask, band_mask);
+                                    p->zone, p->self, (int)p->m, p->imask, band_mask, diag_bits);
   if (c1 > c0)
     k_coarse_exploit<<<(unsigned)((c1 - c0 + kExpWarps - 1) / kExpWarps), kExpWarps * 32, 0,
                        p->stream>>>(P.pass[0], key_col(c), c0, c1, c->imask, true, f, dspan,
-                                    p->zone, p->self, (int)p->m, p->imask, band_mask);
+                                    p->zone, p->self, (int)p->m, p->imask, band_mask, diag_bits);
   p->launches += 2;
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
@@ -564,6 +571,8 @@ mpgpu_plan* mpgpu_plan_create(const double* d_a, int64_t n_a, const double* d_b,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   // attribute is per-device: set it here as well for multi-device processes
   cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
+  cudaFuncSetAttribute(k_join_masked, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(JoinSmem));
   p->n_ctas = sms * std::max(1, g_ctas_per_sm);
   p->coarse_f = coarse_factor(p.get());
   return p.release();
@@ -574,6 +583,8 @@ void mpgpu_plan_destroy(mpgpu_plan* p) {
   cudaSetDevice(p->device);
   cudaStreamSynchronize(p->stream);
   if (p->coarse) mpgpu_plan_destroy(p->coarse);
+  cudaFree(p->d_dmasks);
+  cudaFree(p->d_diag_bits);
   cudaFree(p->xc_a);
   cudaFree(p->xc_b);
   p->A.release();
@@ -766,6 +777,17 @@ mpgpu_status mpgpu_plan_prepare_shard(mpgpu_plan* p, int32_t shard, int32_t n_sh
       cudaGetLastError();
     }
   }
+  if (p->mask_mode && p->coarse_f > 0) {
+    // masked bands: the whole coarse join (the PAA keys only point at fine
+    // diagonals; the exploit then evaluates the chosen ones among them)
+    bool ok = ensure_coarse(p) == MPGPU_OK;
+    if (ok && p->coarse->subset) ok = mpgpu_plan_select_bands(p->coarse, nullptr, -1) == MPGPU_OK;
+    if (ok && coarse_begin(p, 0, 1) == MPGPU_OK) {
+      p->coarse_pending = true;
+    } else {
+      cudaGetLastError();
+    }
+  }
   if (npass > 0 && p->coarse_f > 0) {
     // the coarse phase only tightens the filter: if it cannot run (e.g. the
     // nested plan's allocations fail), the join proceeds without it
@@ -847,6 +869,16 @@ mpgpu_status mpgpu_plan_run(mpgpu_plan* p, int32_t shard, int32_t n_shards) {
   P.n_items = (int)n_mine;
   P.counter = p->d_counter;
   const int grid = (int)std::min<long long>((n_mine + kWarps - 1) / kWarps, p->n_ctas);
+  if (p->mask_mode) {
+    MaskedParams MP;
+    MP.J = P;
+    MP.dmasks = p->d_dmasks;
+    MP.klo = p->zone + 1;
+    k_join_masked<<<grid, kThreads, sizeof(JoinSmem), p->stream>>>(MP);
+    p->launches += 1;
+    MPG_CUDA(cudaGetLastError());
+    return MPGPU_OK;
+  }
   static const bool want_stats = getenv("MPGPU_STATS") && atoi(getenv("MPGPU_STATS")) > 0;
   unsigned long long* d_stats = nullptr;
   if (want_stats) {
@@ -908,6 +940,13 @@ mpgpu_status mpgpu_plan_finalize_shard(mpgpu_plan* p, int32_t shard, int32_t n_s
                                                          (int)p->m, p->imask, d_mp_a,
                                                          (long long*)d_pi_a, (long long*)d_left_a,
                                                          (long long*)d_right_a);
+    p->launches += 1;
+  } else if (p->mask_mode) {
+    if (n_shards != 1) return fail(MPGPU_EUNSUPPORTED, "anytime runs finalize in one piece");
+    const long long thr = p->A.L * 32;
+    k_finalize_self_masked<<<(unsigned)((thr + bs - 1) / bs), bs, 0, p->stream>>>(
+        p->A.view(), key_row(p), key_col(p), (int)p->m, p->imask, p->d_diag_bits, p->d_diags,
+        p->n_diags, d_mp_a, (long long*)d_pi_a, (long long*)d_left_a, (long long*)d_right_a);
     p->launches += 1;
   } else if (p->self && p->subset) {
     if (n_shards != 1) return fail(MPGPU_EUNSUPPORTED, "anytime runs finalize in one piece");
@@ -1075,12 +1114,14 @@ mpgpu_status mpgpu_plan_select_bands(mpgpu_plan* p, const int64_t* band_ids, int
     if (p->subset) p->slice_n = 0;
     p->subset = false;
     p->diag_mode = false;
+    p->mask_mode = false;
     p->bands.clear();
     p->coarse_diags.clear();
     if (p->coarse && p->coarse->subset) mpgpu_plan_select_bands(p->coarse, nullptr, -1);
     return MPGPU_OK;
   }
   p->diag_mode = false;
+  p->mask_mode = false;
   if (!p->self) return fail(MPGPU_EUNSUPPORTED, "band subsets (anytime SCRIMP) are self-join only");
   const long long nb = mpgpu_plan_num_bands(p), klo = p->zone + 1;
   std::vector<long long> kb;
@@ -1214,9 +1255,41 @@ mpgpu_status plan_select_diagonals(mpgpu_plan* p, const std::vector<long long>& 
     p->n_init_diags = (int)wd.size();
   }
   p->bands.clear();
+  p->coarse_diags.clear();
   p->subset = true;
   p->diag_mode = true;
+  p->mask_mode = false;
   p->slice_n = 0;
+  // Dense sets: from about 9% of all diagonals on, nearly every band of kW holds
+  // a chosen one and one diagonal per lane costs more than whole bands. Then the
+  // bands that hold a chosen diagonal run through k_join_masked (the band-subset
+  // machinery with per-lane diagonal masks), and the finalize checks
+  // admissibility per diagonal (k_finalize_self_masked).
+  static const double dense = getenv("MPGPU_MASK_MIN_DENSITY") ? atof(getenv("MPGPU_MASK_MIN_DENSITY")) : 0.09;
+  const long long klo = p->zone + 1, nd = L - klo;
+  if (nd > 0 && !diags.empty() && (double)diags.size() >= dense * (double)nd) {
+    const long long nbt = std::max<long long>(1, mpgpu_plan_num_bands(p));
+    std::vector<unsigned char> dm((size_t)nbt * 32, 0);
+    std::vector<uint32_t> bits((size_t)((L + 31) / 32), 0u);
+    std::vector<long long> kb;
+    for (long long k : diags) {
+      const long long o = k - klo, b = o / kW;
+      dm[(size_t)(b * 32 + (o % kW) / kD)] |= (unsigned char)(1u << (o % kD));
+      bits[(size_t)(k >> 5)] |= 1u << (k & 31);
+      if (kb.empty() || kb.back() != klo + b * kW) kb.push_back(klo + b * kW);  // diags ascend
+    }
+    cudaFree(p->d_dmasks);
+    cudaFree(p->d_diag_bits);
+    p->d_dmasks = nullptr;
+    p->d_diag_bits = nullptr;
+    MPG_CUDA(cudaMalloc(&p->d_dmasks, dm.size()));
+    MPG_CUDA(cudaMemcpy(p->d_dmasks, dm.data(), dm.size(), cudaMemcpyHostToDevice));
+    MPG_CUDA(cudaMalloc(&p->d_diag_bits, sizeof(uint32_t) * bits.size()));
+    MPG_CUDA(cudaMemcpy(p->d_diag_bits, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice));
+    p->bands.swap(kb);
+    p->diag_mode = false;
+    p->mask_mode = true;
+  }
   return MPGPU_OK;
 }
 }  // namespace

@@ -482,6 +482,317 @@ __device__ __forceinline__ bool any_ge(const int (&hc)[kD], const int (&t)[kD]) 
   return r != 0;
 }
 
+// Direct seeds of a band segment: cov(r0, r0 + k) for the band's kW diagonals
+// (the reference's FFT seed row, fft.hpp:49-50), lane t receiving its
+// diagonals t*kD + [0, kD). c0 = r0 + kb.
+__device__ __forceinline__ void seed_direct(WarpSmem& S, const Series& R, const Series& C, long long r0,
+                                            long long c0, int m, int lane, double (&cov)[kD]) {
+  // cov = sum_t a_t (y_t - mu_j) = sum_t a_t y_t - mu_j sum_t a_t with the
+  // row window centred (a_t = x_t - mu_i, sum a_t ~ 0): one DFMA per term.
+  double* ac = reinterpret_cast<double*>(S.colU);       // kSeedChunk
+  double* xc = ac + kSeedChunk;                          // kW + kSeedChunk
+  double* seed = reinterpret_cast<double*>(S.colI);      // kW
+  const double mr = R.mu[r0];
+  double mc[kD], acc[kD];
+#pragma unroll
+  for (int e = 0; e < kD; ++e) {
+    const long long j = c0 + lane + e * 32;
+    mc[e] = j < C.L ? C.mu[j] : 0.0;
+    acc[e] = 0.0;
+  }
+  double asum = 0.0;
+  for (int t0 = 0; t0 < m; t0 += kSeedChunk) {
+    const int tc = min(kSeedChunk, m - t0);
+    for (int q = lane; q < tc; q += 32) ac[q] = R.x[r0 + t0 + q] - mr;
+    for (int q = lane; q < kW + tc; q += 32) {
+      const long long g = c0 + t0 + q;
+      xc[q] = g < C.n ? C.x[g] : 0.0;
+    }
+    __syncwarp();
+    for (int t = 0; t < tc; ++t) {
+      const double a = ac[t];
+      asum += a;
+#pragma unroll
+      for (int e = 0; e < kD; ++e) acc[e] = fma(a, xc[lane + e * 32 + t], acc[e]);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int e = 0; e < kD; ++e) seed[lane + e * 32] = fma(-mc[e], asum, acc[e]);
+  __syncwarp();
+#pragma unroll
+  for (int d = 0; d < kD; ++d) cov[d] = seed[lane * kD + d];
+  __syncwarp();
+}
+
+// A diagonal whose covariance is this NaN (sign bit set) never produces a
+// candidate: DFMA and DMUL propagate the NaN with its sign (measured on
+// sm_100a), so the high word of every "correlation" along it is 0xfff80000, a
+// negative int32 below every filter threshold. k_join_masked seeds the
+// diagonals outside an anytime run's chosen set with it: the fast pass needs no
+// mask at all, only the replay excludes them from its candidates.
+constexpr unsigned long long kMaskedCov = 0xfff8000000000000ULL;
+
+// The walk of one band segment: rows [r0, r0 + nT*kH) of the kW diagonals from
+// kb, starting from the covariances at row r0 in cov (the seed row takes no
+// step). kMasked: dmask holds this lane's chosen diagonals (bit d), the others
+// carry kMaskedCov.
+template <bool kMasked>
+__device__ __forceinline__ void walk_band(WarpSmem& S, const Pass& PS, const int m, const long long imask,
+                                          unsigned long long* const stats, const int lane,
+                                          const long long r0, const long long kb, const int nT,
+                                          double (&cov)[kD], const unsigned dmask) {
+  const Series& R = PS.R;
+  const Series& C = PS.C;
+  const long long c0 = r0 + kb;  // column of (lane 0, d = 0) at row r0
+  // ---- tile 0: rows [0, kH) -> buffer 0, columns [0, kH + kW - 1) ------
+  static_assert(kH >= 1, "tile rows");
+  if constexpr (kH <= 32) {
+    if (lane < kH) fetch_row(S, PS, 0, lane, r0 + lane);
+  } else {
+    for (int h = lane; h < kH; h += 32) fetch_row(S, PS, 0, h, r0 + h);
+  }
+  for (int x = lane; x < kH + kW - 1; x += 32) fetch_col(S, PS, c0, x);
+  cp_async_wait_all();
+  if constexpr (kH <= 32) {
+    if (lane < kH) fix_row(S, PS, 0, lane, r0 + lane, imask);
+  } else {
+    for (int h = lane; h < kH; h += 32) fix_row(S, PS, 0, h, r0 + h, imask);
+  }
+  if (lane == 0) S.rowU[0][0] = make_double2(0.0, 0.0);  // the seed row takes no step
+  for (int x = lane; x < kH + kW - 1; x += 32) fix_col(S, PS, c0, x, imask);
+  __syncwarp();
+
+  double2 cU[kD];
+  double cpk[kD];  // pack_col: perturbed cinv (hi word) + lowered threshold (lo word)
+#pragma unroll
+  for (int d = 0; d < kD - 1; ++d) {  // prime slots 0..D-2 with columns lane*D + d
+    const int a = d * kNB + lane;
+    cU[d] = S.colU[a];
+    cpk[d] = S.colI[a].y;
+  }
+
+#ifdef MPGPU_LANE_STREAMS
+  // Per-lane prefetch streams, set up once per item: the row and column this
+  // lane fetches for tile t + 1 sit at fixed offsets from these pointers
+  // (+ t * kH), and its ring slot advances by kH modulo kRing, so a tile's
+  // prefetch and fix-up need no 64-bit index arithmetic or indexed
+  // parameter loads.
+  const long long rr = r0 + kH + lane, cc = c0 + kH + kW - 1 + lane;
+  const double2* const sRU = R.U + rr;
+  const double* const sRI = R.inv + rr;
+  const long long* const sRK = PS.keyR + rr;
+  const double2* const sCU = C.U + cc;
+  const double* const sCI = C.inv + cc;
+  const long long* const sCK = PS.keyC + cc;
+  const long long rlim = R.L - rr, clim = C.L - cc;  // keys exist while ts < lim
+  int px = (kH + kW - 1 + lane) % kRing;             // ring position of this lane's column
+#endif
+  for (int t = 0; t < nT; ++t) {
+    const int buf = t & 1;
+    const long long ts = (long long)t * kH;
+#ifdef MPGPU_LANE_STREAMS
+    const int pa = (px % kD) * kNB + px / kD;  // ring slot of the prefetched column
+#endif
+    // ---- prefetch tile t+1 (its ring slots held columns retired by now) ----
+    if constexpr (kH <= 32) {
+#ifdef MPGPU_LANE_STREAMS
+      if (t + 1 < nT && lane < kH) {
+        cp_async16(&S.rowU[buf ^ 1][lane], sRU + ts);
+        cp_async8(&S.rowI[buf ^ 1][lane].x, sRI + ts);
+        if (ts < rlim) cp_async8(&S.rowI[buf ^ 1][lane].y, sRK + ts);
+        cp_async16(&S.colU[pa], sCU + ts);
+        cp_async8(&S.colI[pa].x, sCI + ts);
+        if (ts < clim) cp_async8(&S.colI[pa].y, sCK + ts);
+      }
+#else
+      if (t + 1 < nT && lane < kH) {
+        fetch_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane);
+        fetch_col(S, PS, c0, ts + kH + kW - 1 + lane);
+      }
+#endif
+    } else if (t + 1 < nT) {
+#pragma unroll
+      for (int h = lane; h < kH; h += 32) {
+        fetch_row(S, PS, buf ^ 1, h, r0 + ts + kH + h);
+        fetch_col(S, PS, c0, ts + kH + kW - 1 + h);
+      }
+    }
+
+    // ---- compute the tile: kH rows x kD diagonals per lane ----------------
+    // Blocks of kD row-steps run branch-free: each row-step only ORs its
+    // filter result into `anyfire`, so loads and DFMAs of later row-steps
+    // schedule freely across earlier ones. A block in which any lane fired
+    // (a few percent) is replayed from its saved start state with the
+    // per-row-step slow path; the arithmetic of every cell is identical.
+    int b0 = (int)(((unsigned)ts / kD + lane) % (unsigned)kNB);
+    for (int u = 0; u < kH; u += kD) {
+      const int b1 = b0 + 1 == kNB ? 0 : b0 + 1;
+#pragma unroll
+      for (int s0 = 0; s0 < kD; s0 += kBlock) {
+        double covs[kD];
+#pragma unroll
+        for (int d = 0; d < kD; ++d) covs[d] = cov[d];
+        // Fire test: max_d hc[d] >= rthr (3-input integer max) or hc[d] >=
+        // cthr[d] for some d; four predicate accumulators merged at block end.
+        bool fa = false, fb = false, fc = false, fd = false;
+#pragma unroll
+        for (int s = s0; s < s0 + kBlock; ++s) {
+          const int h = u + s;
+          const int sin = (s + kD - 1) % kD;  // slot of the entering column
+          {
+            const int a = sin * kNB + (s == 0 ? b0 : b1);
+            cU[sin] = S.colU[a];
+            cpk[sin] = S.colI[a].y;
+          }
+          const double2 ru = S.rowU[buf][h];
+          const double2 ri = S.rowI[buf][h];
+          const int rthr = __double2hiint(ri.y);
+          int hcs[kD];
+#pragma unroll
+          for (int d = 0; d < kD; ++d) {
+            const int sl = (s + d) % kD;
+            cov[d] = fma(ru.x, cU[sl].y, cov[d]);
+            cov[d] = fma(ru.y, cU[sl].x, cov[d]);
+            hcs[d] = __double2hiint(cov[d] * (ri.x * cpk[sl]));  // rinv*cinv off the cov chain
+          }
+          int rmax;
+          if constexpr (kD == 12) {
+            const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
+            const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
+            const int m3 = __vimax3_s32(hcs[6], hcs[7], hcs[8]);
+            const int m4 = __vimax3_s32(hcs[9], hcs[10], hcs[11]);
+            rmax = __vimax3_s32(m1, m2, max(m3, m4));
+          } else if constexpr (kD == 16) {
+            const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
+            const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
+            const int m3 = __vimax3_s32(hcs[6], hcs[7], hcs[8]);
+            const int m4 = __vimax3_s32(hcs[9], hcs[10], hcs[11]);
+            const int m5 = __vimax3_s32(hcs[12], hcs[13], hcs[14]);
+            rmax = max(__vimax3_s32(m1, m2, m3), __vimax3_s32(m4, m5, hcs[15]));
+          } else if constexpr (kD == 8) {
+            const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
+            const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
+            const int m3 = __vimax3_s32(hcs[6], hcs[7], m1);
+            rmax = max(m2, m3);
+          } else {
+            rmax = max(__vimax3_s32(hcs[0], hcs[1], hcs[2]), hcs[3]);
+          }
+          fa |= rmax >= rthr;
+          bool* acc4[4] = {&fb, &fc, &fd, &fa};
+#pragma unroll
+          for (int d = 0; d < kD; ++d) *acc4[d & 3] |= hcs[d] >= __double2loint(cpk[(s + d) % kD]);
+        }
+        const bool anyfire = (fa | fb) | (fc | fd);
+#ifdef MPGPU_EXPERIMENT_FASTONLY
+        if (anyfire && cov[0] == 12345.0) {  // never: measures the fast blocks alone
+#else
+        if (__builtin_expect(__any_sync(0xffffffffu, anyfire), 0)) {
+#endif
+          // ---- replay the block with exact key updates ---------------------
+          // (exact cinv from the ring; thresholds from the packed low words)
+          if (stats && lane == 0) atomicAdd(&stats[3], 1ull);
+          double cinv[kD];
+          int cthr[kD];
+#pragma unroll
+          for (int d = 0; d < kD; ++d) cov[d] = covs[d];
+#pragma unroll
+          for (int q = 0; q < kD - 1; ++q) {  // block-start window: columns rho0 + lane*kD + q
+            const int a = ((s0 + q) % kD) * kNB + (s0 + q >= kD ? b1 : b0);
+            cU[(s0 + q) % kD] = S.colU[a];
+            const double2 ci = S.colI[a];
+            cinv[(s0 + q) % kD] = ci.x;
+            cthr[(s0 + q) % kD] = __double2loint(ci.y);
+          }
+#pragma unroll
+          for (int s = s0; s < s0 + kBlock; ++s) {
+            const int h = u + s;
+            const int sin = (s + kD - 1) % kD;
+            {
+              const int a = sin * kNB + (s == 0 ? b0 : b1);
+              cU[sin] = S.colU[a];
+              const double2 ci = S.colI[a];
+              cinv[sin] = ci.x;
+              cthr[sin] = __double2loint(ci.y);
+            }
+            const double2 ru = S.rowU[buf][h];
+            const double2 ri = S.rowI[buf][h];
+            const int rthr = __double2hiint(ri.y);
+            SlowIn in;
+            int hcs[kD], tmin[kD];
+#pragma unroll
+            for (int d = 0; d < kD; ++d) {
+              const int sl = (s + d) % kD;
+              cov[d] = fma(ru.x, cU[sl].y, cov[d]);
+              cov[d] = fma(ru.y, cU[sl].x, cov[d]);
+              in.c[d] = cov[d] * (ri.x * cinv[sl]);
+              hcs[d] = __double2hiint(in.c[d]);
+              tmin[d] = min(rthr, cthr[sl]);
+            }
+            const bool fire = any_ge(hcs, tmin);
+            if (__any_sync(0xffffffffu, fire && ri.x != 0.0)) {
+              unsigned live = 0;
+              if (ri.x != 0.0) {
+#pragma unroll
+                for (int d = 0; d < kD; ++d) live |= (cinv[(s + d) % kD] != 0.0 ? 1u : 0u) << d;
+              }
+              if constexpr (kMasked) live &= dmask;
+#pragma unroll
+              for (int d = 0; d < kD; ++d) in.cthr[d] = cthr[(s + d) % kD];
+              const long long rho = ts + h;
+              const SlowOut o = slow_path(in, live, rthr, r0 + rho, rho + (long long)lane * kD, c0,
+                                          h, buf, imask, PS.keyR, PS.keyC, stats);
+#pragma unroll
+              for (int d = 0; d < kD; ++d) cthr[(s + d) % kD] = o.cthr[d];
+            }
+          }
+          // back to the fast pass: packed values of the carried slots (the
+          // slow path may have raised their thresholds in the ring)
+#pragma unroll
+          for (int q = 0; q < kD - 1; ++q) {
+            const int sq_ = (s0 + kBlock + q) % kD;
+            cpk[sq_] = S.colI[sq_ * kNB + (s0 + kBlock + q >= kD ? b1 : b0)].y;
+          }
+        }
+      }
+      b0 = b1;
+    }
+
+    // ---- land the prefetch (warp-local) -------------------------------------
+    if (t + 1 < nT) {
+      cp_async_wait_all();
+      if constexpr (kH <= 32) {
+#ifdef MPGPU_LANE_STREAMS
+        if (lane < kH) {
+          const double2 vr = S.rowI[buf ^ 1][lane];
+          const double tr = (ts < rlim && vr.x != 0.0) ? thr_filter(__double_as_longlong(vr.y), imask) : 2.0;
+          S.rowI[buf ^ 1][lane].y = __hiloint2double(lower_thr(__double2hiint(tr)), 0);
+          const double2 vc = S.colI[pa];
+          const double tc = (ts < clim && vc.x != 0.0) ? thr_filter(__double_as_longlong(vc.y), imask) : 2.0;
+          S.colI[pa].y = pack_col(vc.x, lower_thr(__double2hiint(tc)));
+        }
+#else
+        if (lane < kH) {
+          fix_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane, imask);
+          fix_col(S, PS, c0, ts + kH + kW - 1 + lane, imask);
+        }
+#endif
+      } else {
+#pragma unroll
+        for (int h = lane; h < kH; h += 32) {
+          fix_row(S, PS, buf ^ 1, h, r0 + ts + kH + h, imask);
+          fix_col(S, PS, c0, ts + kH + kW - 1 + h, imask);
+        }
+      }
+    }
+#ifdef MPGPU_LANE_STREAMS
+    px += kH;
+    if (px >= kRing) px -= kRing;
+#endif
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -498,298 +809,46 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_join(const JoinParams 
     if (item_id >= P.n_items) break;
     const Item it = P.items[item_id];
     const Pass& PS = P.pass[it.pass];
-    const Series& R = PS.R;
-    const Series& C = PS.C;
-    const long long r0 = it.r0;
-    const long long c0 = r0 + it.kb;  // column of (lane 0, d = 0) at row r0
-    const int nT = it.nrows / kH;
-
-    // ---- seeds: cov(r0, r0 + k) for the band's kW diagonals --------------
-    // cov = sum_t a_t (y_t - mu_j) = sum_t a_t y_t - mu_j sum_t a_t with the
-    // row window centred (a_t = x_t - mu_i, sum a_t ~ 0): one DFMA per term.
     double cov[kD];
-    {
-      double* ac = reinterpret_cast<double*>(S.colU);       // kSeedChunk
-      double* xc = ac + kSeedChunk;                          // kW + kSeedChunk
-      double* seed = reinterpret_cast<double*>(S.colI);      // kW
-      const double mr = R.mu[r0];
-      double mc[kD], acc[kD];
-#pragma unroll
-      for (int e = 0; e < kD; ++e) {
-        const long long j = c0 + lane + e * 32;
-        mc[e] = j < C.L ? C.mu[j] : 0.0;
-        acc[e] = 0.0;
-      }
-      double asum = 0.0;
-      for (int t0 = 0; t0 < m; t0 += kSeedChunk) {
-        const int tc = min(kSeedChunk, m - t0);
-        for (int q = lane; q < tc; q += 32) ac[q] = R.x[r0 + t0 + q] - mr;
-        for (int q = lane; q < kW + tc; q += 32) {
-          const long long g = c0 + t0 + q;
-          xc[q] = g < C.n ? C.x[g] : 0.0;
-        }
-        __syncwarp();
-        for (int t = 0; t < tc; ++t) {
-          const double a = ac[t];
-          asum += a;
-#pragma unroll
-          for (int e = 0; e < kD; ++e) acc[e] = fma(a, xc[lane + e * 32 + t], acc[e]);
-        }
-        __syncwarp();
-      }
-#pragma unroll
-      for (int e = 0; e < kD; ++e) seed[lane + e * 32] = fma(-mc[e], asum, acc[e]);
-      __syncwarp();
-#pragma unroll
-      for (int d = 0; d < kD; ++d) cov[d] = seed[lane * kD + d];
-      __syncwarp();
-    }
+    seed_direct(S, PS.R, PS.C, it.r0, it.r0 + it.kb, m, lane, cov);
+    walk_band<false>(S, PS, m, imask, P.stats, lane, it.r0, it.kb, it.nrows / kH, cov, 0u);
+  }
+}
 
-    // ---- tile 0: rows [0, kH) -> buffer 0, columns [0, kH + kW - 1) ------
-    static_assert(kH >= 1, "tile rows");
-    if constexpr (kH <= 32) {
-      if (lane < kH) fetch_row(S, PS, 0, lane, r0 + lane);
-    } else {
-      for (int h = lane; h < kH; h += 32) fetch_row(S, PS, 0, h, r0 + h);
-    }
-    for (int x = lane; x < kH + kW - 1; x += 32) fetch_col(S, PS, c0, x);
-    cp_async_wait_all();
-    if constexpr (kH <= 32) {
-      if (lane < kH) fix_row(S, PS, 0, lane, r0 + lane, imask);
-    } else {
-      for (int h = lane; h < kH; h += 32) fix_row(S, PS, 0, h, r0 + h, imask);
-    }
-    if (lane == 0) S.rowU[0][0] = make_double2(0.0, 0.0);  // the seed row takes no step
-    for (int x = lane; x < kH + kW - 1; x += 32) fix_col(S, PS, c0, x, imask);
-    __syncwarp();
+// ---- K3m: the band join over a diagonal SUBSET (exact anytime SCRIMP, dense sets) ----
+// SCRIMP's first s_size diagonals of its seeded order are a
+// random subset. From about 9% of all diagonals on, nearly every band of kW
+// holds some of them, and one diagonal per lane (k_diag_join) costs more than
+// walking whole bands: this kernel is k_join over the bands that hold a chosen
+// diagonal, with the other diagonals masked out (see kMaskedCov). Self-joins
+// only. dmasks: one byte per lane and band, bit d = diagonal klo + 256 band +
+// 8 lane + d is chosen.
+struct MaskedParams {
+  JoinParams J;
+  const unsigned char* dmasks;
+  long long klo;
+};
 
-    double2 cU[kD];
-    double cpk[kD];  // pack_col: perturbed cinv (hi word) + lowered threshold (lo word)
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_join_masked(const MaskedParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  WarpSmem& S = reinterpret_cast<JoinSmem*>(smem_raw)->w[threadIdx.x >> 5];
+  if (lane == 0) S.zero = 0;
+  __syncwarp();
+  for (;;) {
+    int item_id = 0;
+    if (lane == 0) item_id = atomicAdd(P.J.counter, 1);
+    item_id = __shfl_sync(0xffffffffu, item_id, 0);
+    if (item_id >= P.J.n_items) break;
+    const Item it = P.J.items[item_id];
+    const Pass& PS = P.J.pass[0];
+    const unsigned dmask = P.dmasks[((it.kb - P.klo) / kW) * 32 + lane];
+    double cov[kD];
+    seed_direct(S, PS.R, PS.C, it.r0, it.r0 + it.kb, P.J.m, lane, cov);
 #pragma unroll
-    for (int d = 0; d < kD - 1; ++d) {  // prime slots 0..D-2 with columns lane*D + d
-      const int a = d * kNB + lane;
-      cU[d] = S.colU[a];
-      cpk[d] = S.colI[a].y;
-    }
-
-#ifdef MPGPU_LANE_STREAMS
-    // Per-lane prefetch streams, set up once per item: the row and column this
-    // lane fetches for tile t + 1 sit at fixed offsets from these pointers
-    // (+ t * kH), and its ring slot advances by kH modulo kRing, so a tile's
-    // prefetch and fix-up need no 64-bit index arithmetic or indexed
-    // parameter loads.
-    const long long rr = r0 + kH + lane, cc = c0 + kH + kW - 1 + lane;
-    const double2* const sRU = R.U + rr;
-    const double* const sRI = R.inv + rr;
-    const long long* const sRK = PS.keyR + rr;
-    const double2* const sCU = C.U + cc;
-    const double* const sCI = C.inv + cc;
-    const long long* const sCK = PS.keyC + cc;
-    const long long rlim = R.L - rr, clim = C.L - cc;  // keys exist while ts < lim
-    int px = (kH + kW - 1 + lane) % kRing;             // ring position of this lane's column
-#endif
-    for (int t = 0; t < nT; ++t) {
-      const int buf = t & 1;
-      const long long ts = (long long)t * kH;
-#ifdef MPGPU_LANE_STREAMS
-      const int pa = (px % kD) * kNB + px / kD;  // ring slot of the prefetched column
-#endif
-      // ---- prefetch tile t+1 (its ring slots held columns retired by now) ----
-      if constexpr (kH <= 32) {
-#ifdef MPGPU_LANE_STREAMS
-        if (t + 1 < nT && lane < kH) {
-          cp_async16(&S.rowU[buf ^ 1][lane], sRU + ts);
-          cp_async8(&S.rowI[buf ^ 1][lane].x, sRI + ts);
-          if (ts < rlim) cp_async8(&S.rowI[buf ^ 1][lane].y, sRK + ts);
-          cp_async16(&S.colU[pa], sCU + ts);
-          cp_async8(&S.colI[pa].x, sCI + ts);
-          if (ts < clim) cp_async8(&S.colI[pa].y, sCK + ts);
-        }
-#else
-        if (t + 1 < nT && lane < kH) {
-          fetch_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane);
-          fetch_col(S, PS, c0, ts + kH + kW - 1 + lane);
-        }
-#endif
-      } else if (t + 1 < nT) {
-#pragma unroll
-        for (int h = lane; h < kH; h += 32) {
-          fetch_row(S, PS, buf ^ 1, h, r0 + ts + kH + h);
-          fetch_col(S, PS, c0, ts + kH + kW - 1 + h);
-        }
-      }
-
-      // ---- compute the tile: kH rows x kD diagonals per lane ----------------
-      // Blocks of kD row-steps run branch-free: each row-step only ORs its
-      // filter result into `anyfire`, so loads and DFMAs of later row-steps
-      // schedule freely across earlier ones. A block in which any lane fired
-      // (a few percent) is replayed from its saved start state with the
-      // per-row-step slow path; the arithmetic of every cell is identical.
-      int b0 = (int)(((unsigned)ts / kD + lane) % (unsigned)kNB);
-      for (int u = 0; u < kH; u += kD) {
-        const int b1 = b0 + 1 == kNB ? 0 : b0 + 1;
-#pragma unroll
-        for (int s0 = 0; s0 < kD; s0 += kBlock) {
-          double covs[kD];
-#pragma unroll
-          for (int d = 0; d < kD; ++d) covs[d] = cov[d];
-          // Fire test: max_d hc[d] >= rthr (3-input integer max) or hc[d] >=
-          // cthr[d] for some d; four predicate accumulators merged at block end.
-          bool fa = false, fb = false, fc = false, fd = false;
-#pragma unroll
-          for (int s = s0; s < s0 + kBlock; ++s) {
-            const int h = u + s;
-            const int sin = (s + kD - 1) % kD;  // slot of the entering column
-            {
-              const int a = sin * kNB + (s == 0 ? b0 : b1);
-              cU[sin] = S.colU[a];
-              cpk[sin] = S.colI[a].y;
-            }
-            const double2 ru = S.rowU[buf][h];
-            const double2 ri = S.rowI[buf][h];
-            const int rthr = __double2hiint(ri.y);
-            int hcs[kD];
-#pragma unroll
-            for (int d = 0; d < kD; ++d) {
-              const int sl = (s + d) % kD;
-              cov[d] = fma(ru.x, cU[sl].y, cov[d]);
-              cov[d] = fma(ru.y, cU[sl].x, cov[d]);
-              hcs[d] = __double2hiint(cov[d] * (ri.x * cpk[sl]));  // rinv*cinv off the cov chain
-            }
-            int rmax;
-            if constexpr (kD == 12) {
-              const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
-              const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
-              const int m3 = __vimax3_s32(hcs[6], hcs[7], hcs[8]);
-              const int m4 = __vimax3_s32(hcs[9], hcs[10], hcs[11]);
-              rmax = __vimax3_s32(m1, m2, max(m3, m4));
-            } else if constexpr (kD == 16) {
-              const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
-              const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
-              const int m3 = __vimax3_s32(hcs[6], hcs[7], hcs[8]);
-              const int m4 = __vimax3_s32(hcs[9], hcs[10], hcs[11]);
-              const int m5 = __vimax3_s32(hcs[12], hcs[13], hcs[14]);
-              rmax = max(__vimax3_s32(m1, m2, m3), __vimax3_s32(m4, m5, hcs[15]));
-            } else if constexpr (kD == 8) {
-              const int m1 = __vimax3_s32(hcs[0], hcs[1], hcs[2]);
-              const int m2 = __vimax3_s32(hcs[3], hcs[4], hcs[5]);
-              const int m3 = __vimax3_s32(hcs[6], hcs[7], m1);
-              rmax = max(m2, m3);
-            } else {
-              rmax = max(__vimax3_s32(hcs[0], hcs[1], hcs[2]), hcs[3]);
-            }
-            fa |= rmax >= rthr;
-            bool* acc4[4] = {&fb, &fc, &fd, &fa};
-#pragma unroll
-            for (int d = 0; d < kD; ++d) *acc4[d & 3] |= hcs[d] >= __double2loint(cpk[(s + d) % kD]);
-          }
-          const bool anyfire = (fa | fb) | (fc | fd);
-#ifdef MPGPU_EXPERIMENT_FASTONLY
-          if (anyfire && cov[0] == 12345.0) {  // never: measures the fast blocks alone
-#else
-          if (__builtin_expect(__any_sync(0xffffffffu, anyfire), 0)) {
-#endif
-            // ---- replay the block with exact key updates ---------------------
-            // (exact cinv from the ring; thresholds from the packed low words)
-            if (P.stats && lane == 0) atomicAdd(&P.stats[3], 1ull);
-            double cinv[kD];
-            int cthr[kD];
-#pragma unroll
-            for (int d = 0; d < kD; ++d) cov[d] = covs[d];
-#pragma unroll
-            for (int q = 0; q < kD - 1; ++q) {  // block-start window: columns rho0 + lane*kD + q
-              const int a = ((s0 + q) % kD) * kNB + (s0 + q >= kD ? b1 : b0);
-              cU[(s0 + q) % kD] = S.colU[a];
-              const double2 ci = S.colI[a];
-              cinv[(s0 + q) % kD] = ci.x;
-              cthr[(s0 + q) % kD] = __double2loint(ci.y);
-            }
-#pragma unroll
-            for (int s = s0; s < s0 + kBlock; ++s) {
-              const int h = u + s;
-              const int sin = (s + kD - 1) % kD;
-              {
-                const int a = sin * kNB + (s == 0 ? b0 : b1);
-                cU[sin] = S.colU[a];
-                const double2 ci = S.colI[a];
-                cinv[sin] = ci.x;
-                cthr[sin] = __double2loint(ci.y);
-              }
-              const double2 ru = S.rowU[buf][h];
-              const double2 ri = S.rowI[buf][h];
-              const int rthr = __double2hiint(ri.y);
-              SlowIn in;
-              int hcs[kD], tmin[kD];
-#pragma unroll
-              for (int d = 0; d < kD; ++d) {
-                const int sl = (s + d) % kD;
-                cov[d] = fma(ru.x, cU[sl].y, cov[d]);
-                cov[d] = fma(ru.y, cU[sl].x, cov[d]);
-                in.c[d] = cov[d] * (ri.x * cinv[sl]);
-                hcs[d] = __double2hiint(in.c[d]);
-                tmin[d] = min(rthr, cthr[sl]);
-              }
-              const bool fire = any_ge(hcs, tmin);
-              if (__any_sync(0xffffffffu, fire && ri.x != 0.0)) {
-                unsigned live = 0;
-                if (ri.x != 0.0) {
-#pragma unroll
-                  for (int d = 0; d < kD; ++d) live |= (cinv[(s + d) % kD] != 0.0 ? 1u : 0u) << d;
-                }
-#pragma unroll
-                for (int d = 0; d < kD; ++d) in.cthr[d] = cthr[(s + d) % kD];
-                const long long rho = ts + h;
-                const SlowOut o = slow_path(in, live, rthr, r0 + rho, rho + (long long)lane * kD, c0,
-                                            h, buf, imask, PS.keyR, PS.keyC, P.stats);
-#pragma unroll
-                for (int d = 0; d < kD; ++d) cthr[(s + d) % kD] = o.cthr[d];
-              }
-            }
-            // back to the fast pass: packed values of the carried slots (the
-            // slow path may have raised their thresholds in the ring)
-#pragma unroll
-            for (int q = 0; q < kD - 1; ++q) {
-              const int sq_ = (s0 + kBlock + q) % kD;
-              cpk[sq_] = S.colI[sq_ * kNB + (s0 + kBlock + q >= kD ? b1 : b0)].y;
-            }
-          }
-        }
-        b0 = b1;
-      }
-
-      // ---- land the prefetch (warp-local) -------------------------------------
-      if (t + 1 < nT) {
-        cp_async_wait_all();
-        if constexpr (kH <= 32) {
-#ifdef MPGPU_LANE_STREAMS
-          if (lane < kH) {
-            const double2 vr = S.rowI[buf ^ 1][lane];
-            const double tr = (ts < rlim && vr.x != 0.0) ? thr_filter(__double_as_longlong(vr.y), imask) : 2.0;
-            S.rowI[buf ^ 1][lane].y = __hiloint2double(lower_thr(__double2hiint(tr)), 0);
-            const double2 vc = S.colI[pa];
-            const double tc = (ts < clim && vc.x != 0.0) ? thr_filter(__double_as_longlong(vc.y), imask) : 2.0;
-            S.colI[pa].y = pack_col(vc.x, lower_thr(__double2hiint(tc)));
-          }
-#else
-          if (lane < kH) {
-            fix_row(S, PS, buf ^ 1, lane, r0 + ts + kH + lane, imask);
-            fix_col(S, PS, c0, ts + kH + kW - 1 + lane, imask);
-          }
-#endif
-        } else {
-#pragma unroll
-          for (int h = lane; h < kH; h += 32) {
-            fix_row(S, PS, buf ^ 1, h, r0 + ts + kH + h, imask);
-            fix_col(S, PS, c0, ts + kH + kW - 1 + h, imask);
-          }
-        }
-      }
-#ifdef MPGPU_LANE_STREAMS
-      px += kH;
-      if (px >= kRing) px -= kRing;
-#endif
-      __syncwarp();
-    }
+    for (int d = 0; d < kD; ++d)
+      if (!((dmask >> d) & 1u)) cov[d] = __longlong_as_double((long long)kMaskedCov);
+    walk_band<true>(S, PS, P.J.m, P.J.imask, P.J.stats, lane, it.r0, it.kb, it.nrows / kH, cov, dmask);
   }
 }
 
@@ -1051,7 +1110,7 @@ struct ExpSmem {
 __global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
     const Pass PS, const long long* __restrict__ ckey, long long I0, long long I1, long long cimask,
     bool key_is_col, int f, int span, long long zone, bool self, int m, long long imask,
-    const unsigned* __restrict__ band_mask) {
+    const unsigned* __restrict__ band_mask, const unsigned* __restrict__ diag_bits) {
   __shared__ ExpSmem sm[kExpWarps];
   ExpSmem& S = sm[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1122,6 +1181,10 @@ __global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
       if (band_mask && q0 < qn) {  // anytime band subset: only the chosen bands' diagonals
         const long long b = (j0 - i0 - zone - 1) / kW;
         if (!((band_mask[b >> 5] >> (b & 31)) & 1u)) q0 = qn = 0;
+      }
+      if (diag_bits && q0 < qn) {  // anytime diagonal subset (masked bands): chosen diagonals only
+        const long long k = j0 - i0;
+        if (!((diag_bits[k >> 5] >> (k & 31)) & 1u)) q0 = qn = 0;
       }
       q0s[g] = q0;
       qns[g] = qn;
@@ -1714,6 +1777,89 @@ __global__ void k_finalize_self_partial(const Series A, const long long* __restr
   const long long bi = best == kKeyNone ? -1 : (best & imask);
   // every 8-lane group computes the same value, in the same order as the full
   // join's finalize (so a full-coverage neighbour gets bit-identical values)
+  const double v = group_value(A, i, A, bi, true, m, lane % kFinLanes);
+  if (lane == 0) {
+    if (mp) mp[i] = v;
+    if (pi) pi[i] = bi;
+    if (left) left[i] = -1;
+    if (right) right[i] = -1;
+  }
+}
+
+// Finalize of a masked band join (exact anytime SCRIMP, dense sets): as
+// k_finalize_self_partial, with admissibility per DIAGONAL. dbits: bit k set
+// when diagonal k is chosen; diags: the chosen diagonals, ascending. The flat
+// convention needs, on either side of row i, the smallest flat window on a
+// chosen diagonal and the smallest admissible neighbour at all. One warp per
+// row: it walks the non-empty words of the flat bitmask (next_word skips the
+// rest), one window per lane, and stops at the first word with a hit.
+__global__ void k_finalize_self_masked(const Series A, const long long* __restrict__ key_right,
+                                       const long long* __restrict__ key_left, int m, long long imask,
+                                       const uint32_t* __restrict__ dbits,
+                                       const long long* __restrict__ diags, long long n_diags,
+                                       double* __restrict__ mp, long long* __restrict__ pi,
+                                       long long* __restrict__ left, long long* __restrict__ right) {
+  const long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= A.L) return;
+  const long long L = A.L;
+  long long rk = key_right[i], lk = key_left[i];
+  const bool fi = A.inv[i] == 0.0;
+  auto chosen = [&](long long k) { return k >= 0 && k < L && ((dbits[k >> 5] >> (k & 31)) & 1u); };
+  long long rflat = -1, rany = -1, lflat = -1, lany = -1;
+  if (n_diags > 0 && next_flat(A, 0) >= 0) {
+    const long long kmin = diags[0];
+    if (i + kmin < L) rany = i + kmin;
+    // the largest chosen diagonal <= i gives the smallest left neighbour
+    {
+      long long lo = 0, hi = n_diags;  // first index with diags[idx] > i
+      while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (diags[mid] <= i) lo = mid + 1; else hi = mid;
+      }
+      if (lo > 0) lany = i - diags[lo - 1];
+    }
+    // right: flat windows j >= i + kmin, ascending
+    if (rany >= 0) {
+      int w = A.next_word[rany >> 5];
+      while (w >= 0) {
+        const long long j = ((long long)w << 5) + lane;
+        const bool hit = ((A.flat_words[w] >> lane) & 1u) && j >= rany && j < L && chosen(j - i);
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (b) { rflat = ((long long)w << 5) + __ffs(b) - 1; break; }
+        w = w + 1 < A.n_words ? A.next_word[w + 1] : -1;
+      }
+    }
+    // left: flat windows j <= i - kmin, ascending from 0
+    if (lany >= 0) {
+      const long long jmax = i - kmin;
+      int w = A.next_word[0];
+      while (w >= 0 && ((long long)w << 5) <= jmax) {
+        const long long j = ((long long)w << 5) + lane;
+        const bool hit = ((A.flat_words[w] >> lane) & 1u) && j <= jmax && chosen(i - j);
+        const unsigned b = __ballot_sync(0xffffffffu, hit);
+        if (b) { lflat = ((long long)w << 5) + __ffs(b) - 1; break; }
+        w = w + 1 < A.n_words ? A.next_word[w + 1] : -1;
+      }
+    }
+  }
+  if (fi) {
+    rk = rflat >= 0 ? mk_key_score(0.0, rflat, imask)
+                    : (rany >= 0 ? mk_key_score(0.5, rany, imask) : kKeyNone);
+    lk = lflat >= 0 ? mk_key_score(0.0, lflat, imask)
+                    : (lany >= 0 ? mk_key_score(0.5, lany, imask) : kKeyNone);
+  } else {
+    if (rflat >= 0) {
+      const long long k = mk_key_score(0.5, rflat, imask);
+      rk = k < rk ? k : rk;
+    }
+    if (lflat >= 0) {
+      const long long k = mk_key_score(0.5, lflat, imask);
+      lk = k < lk ? k : lk;
+    }
+  }
+  const long long best = lk <= rk ? lk : rk;
+  const long long bi = best == kKeyNone ? -1 : (best & imask);
   const double v = group_value(A, i, A, bi, true, m, lane % kFinLanes);
   if (lane == 0) {
     if (mp) mp[i] = v;

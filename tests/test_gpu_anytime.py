@@ -79,11 +79,15 @@ def test_anytime_monotone_and_full(mp, gran):
 
 
 @pytest.mark.parametrize("n,w,ez,frac,seed", [(30000, 64, 0.5, 0.1, 1), (12000, 50, 0.25, 0.37, 5),
-                                             (5000, 32, 0.5, 1e-4, 3), (40000, 128, 0.5, 0.02, 11)])
+                                             (5000, 32, 0.5, 1e-4, 3), (40000, 128, 0.5, 0.02, 11),
+                                             (30000, 64, 0.5, 0.6, 4), (9000, 40, 0.5, 0.97, 8),
+                                             (70000, 256, 0.5, 0.09, 2)])
 def test_exact_mode_matches_oracle_scrimp(mp, oracle_lib, n, w, ez, frac, seed):
     """The reference's SCRIMP semantics: the GPU evaluates exactly the oracle's
     first s_size diagonals of the seeded order (s_size = 1 included), so the
-    partial profiles agree with or_scrimp itself; coverage is s_size / total."""
+    partial profiles agree with or_scrimp itself; coverage is s_size / total.
+    Below 9% of the diagonals that is k_diag_join (one diagonal per lane), from
+    9% on k_join_masked over the bands that hold a chosen diagonal."""
     g = np.random.default_rng(seed)
     x = np.cumsum(g.standard_normal(n))
     x[n // 5:n // 5 + 3 * w] = x[n // 5]      # a flat run: the convention inside the subset
