@@ -117,3 +117,33 @@ def test_exact_mode_via_cpp_default(mp, oracle_lib):
     r = mp.scrimp(x, 40, 0.5, s_size=777, seed=2)
     ref_mp = oracle_lib.scrimp(x, 40, 0.5, s_size=777, seed=2)[0]
     assert close(r.values, ref_mp)[0] and r.coverage == 777 / (8000 - 40 + 1 - 20 - 1)
+
+
+def test_masked_bands_and_per_lane_diagonals_give_the_same_profile(mp, tmp_path):
+    """The two exact-mode kernels on one dense set (30% of the diagonals, flat
+    runs included): k_join_masked in this process, k_diag_join in a child
+    process (MPGPU_MASK_MIN_DENSITY=2 is read once per process). Same values
+    within the parity tolerance, same neighbours up to near-ties."""
+    import os
+    import subprocess
+    import sys
+    n, w, ez, seed = 1 << 17, 128, 0.5, 13
+    x = np.cumsum(np.random.default_rng(21).standard_normal(n))
+    x[3000:3000 + 4 * w] = x[3000]
+    x[90000:90000 + 2 * w] = -1.5
+    nd = n - w + 1 - mp.zone_size(w, ez) - 1
+    s_size = int(0.3 * nd)
+    np.save(tmp_path / "x.npy", x)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    child = (f"import sys, numpy as np; sys.path.insert(0, {root!r}); import paper_1904_12626_b200 as mp; "
+             f"x = np.load({str(tmp_path / 'x.npy')!r}); "
+             f"r = mp.scrimp(x, {w}, {ez}, s_size={s_size}, seed={seed}); "
+             f"np.savez({str(tmp_path / 'lane.npz')!r}, v=r.values, i=r.index)")
+    env = dict(os.environ, MPGPU_MASK_MIN_DENSITY="2")
+    subprocess.run([sys.executable, "-c", child], check=True, env=env, timeout=600)
+    lane = np.load(tmp_path / "lane.npz")
+    r = mp.scrimp(x, w, ez, s_size=s_size, seed=seed)
+    ok, rel = close(r.values, lane["v"])
+    assert ok, f"masked bands vs per-lane diagonals: MP differs (max rel {rel:.3e})"
+    assert not index_mismatches(r.index, lane["i"], np.arange(r.values.size), x, x, w)
+    assert np.array_equal(np.isinf(r.values), np.isinf(lane["v"]))
