@@ -1410,20 +1410,40 @@ mpgpu_status mpgpu_distance_profiles(const double* d_ts, int64_t n, int64_t wind
   std::unique_lock<std::mutex> lk;
   char* scratch = nullptr;
   if (mpgpu_status e = scratch_acquire(device, kScratchMass,
-                                       sizeof(double) * (2 * L + 3 * n_queries), st, lk, &scratch);
+                                       sizeof(double) * (2 * L + 3 * n_queries + kMassConst), st, lk,
+                                       &scratch);
       e != MPGPU_OK)
     return e;
   double* mu = reinterpret_cast<double*>(scratch);
   double* inv = mu + L;
   double* qstat = inv + L;
+  double* stage = qstat + 3 * n_queries;
   k_window_stats<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(d_ts, L, (int)window, mu, inv,
                                                               nullptr, nullptr);
   k_query_stats<<<(unsigned)((n_queries + 127) / 128), 128, 0, st>>>(
       d_ts, d_queries, (const long long*)d_query_pos, (int)n_queries, (int)window, qstat);
-  dim3 grid((unsigned)((L + kMassTile - 1) / kMassTile), (unsigned)n_queries);
-  k_mass<<<grid, kMassThreads, 0, st>>>(d_ts, n, mu, inv, L, (int)window, d_queries,
-                                        (const long long*)d_query_pos, qstat,
-                                        zone < 0 ? -1 : zone, d_out);
+  const unsigned gx = (unsigned)((L + kMassTile - 1) / kMassTile);
+  const int mpad = (int)((window + kMassR - 1) / kMassR * kMassR);
+  static const bool use_const = !(getenv("MPGPU_MASS_CONST") && atoi(getenv("MPGPU_MASS_CONST")) == 0);
+  if (use_const && mpad <= kMassConst) {
+    // the centred queries through constant memory, as many per launch as fit
+    // (the scratch lock and its event order the launches that share c_mass_q)
+    const int per = kMassConst / mpad;
+    for (long long q0 = 0; q0 < n_queries; q0 += per) {
+      const int nq = (int)std::min<long long>(per, n_queries - q0);
+      k_mass_stage<<<(unsigned)((nq * mpad + 255) / 256), 256, 0, st>>>(
+          d_ts, d_queries, (const long long*)d_query_pos, qstat, (int)q0, nq, (int)window, mpad, stage);
+      MPG_CUDA(cudaMemcpyToSymbolAsync(c_mass_q, stage, sizeof(double) * nq * mpad, 0,
+                                       cudaMemcpyDeviceToDevice, st));
+      k_mass<true><<<dim3(gx, (unsigned)nq), kMassThreads, 0, st>>>(
+          d_ts, n, mu, inv, L, (int)window, d_queries, (const long long*)d_query_pos, qstat,
+          zone < 0 ? -1 : zone, d_out, (int)q0, mpad);
+    }
+  } else {
+    k_mass<false><<<dim3(gx, (unsigned)n_queries), kMassThreads, 0, st>>>(
+        d_ts, n, mu, inv, L, (int)window, d_queries, (const long long*)d_query_pos, qstat,
+        zone < 0 ? -1 : zone, d_out, 0, mpad);
+  }
   MPG_CUDA(cudaGetLastError());
   return scratch_release(device, kScratchMass, st);
 }

@@ -1262,8 +1262,14 @@ __global__ void __launch_bounds__(kExpWarps * 32) k_coarse_exploit(
 // kMassR consecutive outputs and slides a register window over the staged
 // series (1 shared load per kMassR DFMAs). Near-zero hits are recomputed
 // directly so exact matches come out as 0 (distance.hpp:30-33).
-constexpr int kMassThreads = 128;
-constexpr int kMassR = 8;
+#ifndef MPGPU_MASS_THREADS
+#define MPGPU_MASS_THREADS 128
+#endif
+constexpr int kMassThreads = MPGPU_MASS_THREADS;
+#ifndef MPGPU_MASS_R
+#define MPGPU_MASS_R 16
+#endif
+constexpr int kMassR = MPGPU_MASS_R;
 constexpr int kMassTile = kMassThreads * kMassR;  // outputs per CTA (1024)
 constexpr int kMassChunk = 512;                   // query samples staged per pass
 static_assert(kMassChunk % kMassR == 0, "query chunks in whole register-window rotations");
@@ -1299,14 +1305,38 @@ __global__ void k_query_stats(const double* __restrict__ x, const double* __rest
   qstat[3 * q + 2] = asum;
 }
 
+// The query sample is the operand all lanes (and a thread's kMassR outputs)
+// share. From shared memory it is a vector register, and a DFMA with three
+// vector-register sources is bound by register-file reads on sm_100 (DESIGN.md
+// §6); from constant memory at a uniform index it is a uniform-register
+// operand. So the centred queries of a launch are staged in c_mass_q (56 KB;
+// k_mass_stage + a device-to-device copy into the symbol), kConst = true, as
+// many queries per launch as fit; windows too long for it keep the
+// shared-memory form.
+constexpr int kMassConst = 7168;
+__constant__ double c_mass_q[kMassConst];
+
+// stage[qc * mpad + t] = query (q0 + qc)'s sample t, centred; 0 for t in [m, mpad)
+__global__ void k_mass_stage(const double* __restrict__ x, const double* __restrict__ queries,
+                             const long long* __restrict__ qpos, const double* __restrict__ qstat,
+                             int q0, int nq, int m, int mpad, double* __restrict__ stage) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nq * mpad) return;
+  const int qc = idx / mpad, t = idx - qc * mpad, q = q0 + qc;
+  const double* qx = queries ? queries + (long long)q * m : x + qpos[q];
+  stage[idx] = t < m ? qx[t] - qstat[3 * q + 0] : 0.0;
+}
+
+template <bool kConst>
 __global__ void __launch_bounds__(kMassThreads) k_mass(
     const double* __restrict__ x, long long n, const double* __restrict__ mu,
     const double* __restrict__ inv, long long L, int m, const double* __restrict__ queries,
     const long long* __restrict__ qpos, const double* __restrict__ qstat, long long zone,
-    double* __restrict__ out) {
-  __shared__ double sq[kMassChunk];
+    double* __restrict__ out, int q0, int mpad) {
+  __shared__ double sq[kConst ? 1 : kMassChunk];
   __shared__ double sx[kMassSxPad];
-  const int q = blockIdx.y;
+  const int q = q0 + blockIdx.y;
+  const int qoff = blockIdx.y * mpad;  // kConst: this query's samples in c_mass_q (uniform)
   const long long j0 = (long long)blockIdx.x * kMassTile;
   const int tid = threadIdx.x;
   const double* qx = queries ? queries + (long long)q * m : x + qpos[q];
@@ -1318,7 +1348,8 @@ __global__ void __launch_bounds__(kMassThreads) k_mass(
   for (int t0 = 0; t0 < m; t0 += kMassChunk) {
     const int tc = min(kMassChunk, m - t0);
     const int tcp = (tc + kMassR - 1) / kMassR * kMassR;  // zero-padded query tail
-    for (int t = tid; t < tcp; t += kMassThreads) sq[t] = t < tc ? qx[t0 + t] - qmean : 0.0;
+    if constexpr (!kConst)
+      for (int t = tid; t < tcp; t += kMassThreads) sq[t] = t < tc ? qx[t0 + t] - qmean : 0.0;
     for (int t = tid; t < kMassTile + tcp; t += kMassThreads) {
       const long long g = j0 + t0 + t;
       sx[mass_pad(t)] = g < n ? x[g] : 0.0;
@@ -1331,7 +1362,7 @@ __global__ void __launch_bounds__(kMassThreads) k_mass(
     for (int t8 = 0; t8 < tcp; t8 += kMassR) {
 #pragma unroll
       for (int s = 0; s < kMassR; ++s) {
-        const double a = sq[t8 + s];
+        const double a = kConst ? c_mass_q[qoff + t0 + t8 + s] : sq[t8 + s];
 #pragma unroll
         for (int r = 0; r < kMassR; ++r) acc[r] = fma(a, w[(s + r) % kMassR], acc[r]);
         w[s] = sx[mass_pad(jl + kMassR + t8 + s)];  // x[jl + t + 8] replaces x[jl + t]
