@@ -1420,7 +1420,7 @@ mpgpu_status mpgpu_distance_profiles(const double* d_ts, int64_t n, int64_t wind
   double* stage = qstat + 3 * n_queries;
   k_window_stats<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(d_ts, L, (int)window, mu, inv,
                                                               nullptr, nullptr);
-  k_query_stats<<<(unsigned)((n_queries + 127) / 128), 128, 0, st>>>(
+  k_query_stats<<<(unsigned)((n_queries + kQStatWarps - 1) / kQStatWarps), kQStatWarps * 32, 0, st>>>(
       d_ts, d_queries, (const long long*)d_query_pos, (int)n_queries, (int)window, qstat);
   const unsigned gx = (unsigned)((L + kMassTile - 1) / kMassTile);
   const int mpad = (int)((window + kMassR - 1) / kMassR * kMassR);

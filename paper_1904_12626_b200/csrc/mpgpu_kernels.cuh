@@ -1283,26 +1283,49 @@ constexpr int kMassSxPad = kMassSx + kMassSx / kMassR + 1;
 // the sum of the centred samples, with the same sequential two-pass as K1, so
 // a query equal to a window of the series gets bit-identical statistics
 // (exact 0 on self-matches).
-__global__ void k_query_stats(const double* __restrict__ x, const double* __restrict__ queries,
-                              const long long* __restrict__ qpos, int n_queries, int m,
-                              double* __restrict__ qstat) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= n_queries) return;
+// One warp per query: the lanes stage the query in shared memory (parallel
+// loads), lane 0 then adds in K1's sequential order, so the sums are bit for
+// bit those of a thread walking the window alone.
+constexpr int kQStatChunk = 1024;
+constexpr int kQStatWarps = 4;
+__global__ void __launch_bounds__(kQStatWarps * 32) k_query_stats(
+    const double* __restrict__ x, const double* __restrict__ queries,
+    const long long* __restrict__ qpos, int n_queries, int m, double* __restrict__ qstat) {
+  __shared__ double buf[kQStatWarps][kQStatChunk];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q = blockIdx.x * kQStatWarps + w;
+  if (q >= n_queries) return;  // whole warp
   const double* qx = queries ? queries + (long long)q * m : x + qpos[q];
   double s = 0.0;
-  for (int t = 0; t < m; ++t) s += qx[t];
-  const double mean = s / (double)m;
-  double ss = 0.0, asum = 0.0;
-  for (int t = 0; t < m; ++t) {
-    const double d = qx[t] - mean;
-    ss = fma(d, d, ss);
-    asum += d;
+  for (int t0 = 0; t0 < m; t0 += kQStatChunk) {
+    const int tc = min(kQStatChunk, m - t0);
+    for (int t = lane; t < tc; t += 32) buf[w][t] = qx[t0 + t];
+    __syncwarp();
+    if (lane == 0)
+      for (int t = 0; t < tc; ++t) s += buf[w][t];
+    __syncwarp();
   }
-  const double sd = sqrt(ss / (double)m);
-  const double scale = fabs(mean) > 1.0 ? fabs(mean) : 1.0;
-  qstat[3 * q + 0] = mean;
-  qstat[3 * q + 1] = sd <= 1e-10 * scale ? 0.0 : 1.0 / sqrt(ss);
-  qstat[3 * q + 2] = asum;
+  const double mean = __shfl_sync(0xffffffffu, s, 0) / (double)m;
+  double ss = 0.0, asum = 0.0;
+  for (int t0 = 0; t0 < m; t0 += kQStatChunk) {
+    const int tc = min(kQStatChunk, m - t0);
+    for (int t = lane; t < tc; t += 32) buf[w][t] = qx[t0 + t];
+    __syncwarp();
+    if (lane == 0)
+      for (int t = 0; t < tc; ++t) {
+        const double d = buf[w][t] - mean;
+        ss = fma(d, d, ss);
+        asum += d;
+      }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    const double sd = sqrt(ss / (double)m);
+    const double scale = fabs(mean) > 1.0 ? fabs(mean) : 1.0;
+    qstat[3 * q + 0] = mean;
+    qstat[3 * q + 1] = sd <= 1e-10 * scale ? 0.0 : 1.0 / sqrt(ss);
+    qstat[3 * q + 2] = asum;
+  }
 }
 
 // The query sample is the operand all lanes (and a thread's kMassR outputs)
