@@ -186,10 +186,20 @@ mpgpu_status alloc_series(DevSeries& s, const double* x, long long n, long long 
   return MPGPU_OK;
 }
 
+// K1 launch: the blocked kernel when the series fills the GPU with its 1024-window CTAs
+static void launch_window_stats(const double* x, long long L, int m, double* mu, double* inv,
+                                double* sd, uint8_t* flat, cudaStream_t st) {
+  if (L >= 2LL * 148 * kStatTile) {
+    k_window_stats_blocked<<<(unsigned)((L + kStatTile - 1) / kStatTile), kStatThreads, 0, st>>>(
+        x, L, m, mu, inv, sd, flat);
+  } else {
+    k_window_stats<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(x, L, m, mu, inv, sd, flat);
+  }
+}
+
 mpgpu_status launch_stats(mpgpu_plan* p, DevSeries& s) {
   const int bs = 256;
-  k_window_stats<<<(unsigned)((s.L + bs - 1) / bs), bs, 0, p->stream>>>(s.x, s.L, (int)p->m, s.mu,
-                                                                          s.inv, nullptr, s.flat);
+  launch_window_stats(s.x, s.L, (int)p->m, s.mu, s.inv, nullptr, s.flat, p->stream);
   k_update_vectors<<<(unsigned)((s.L + kPad + bs - 1) / bs), bs, 0, p->stream>>>(
       s.x, s.mu, s.L, (int)p->m, s.U, s.inv);
   k_flat_words<<<(unsigned)((s.n_words * 32LL + bs - 1) / bs), bs, 0, p->stream>>>(
@@ -461,7 +471,7 @@ cudaError_t series_stats(const double* d_x, long long n, int m, double* mu, doub
                          double2* U, uint8_t* flat, cudaStream_t st) {
   const long long L = n - m + 1;
   const int bs = 256;
-  k_window_stats<<<(unsigned)((L + bs - 1) / bs), bs, 0, st>>>(d_x, L, m, mu, inv, nullptr, flat);
+  launch_window_stats(d_x, L, m, mu, inv, nullptr, flat, st);
   k_update_vectors<<<(unsigned)((L + kPad + bs - 1) / bs), bs, 0, st>>>(d_x, mu, L, m, U, inv);
   return cudaGetLastError();
 }
@@ -503,8 +513,7 @@ mpgpu_status mpgpu_rolling_stats(const double* d_ts, int64_t n, int64_t window, 
   MPG_CUDA(cudaSetDevice(device));
   const long long L = n - window + 1;
   cudaStream_t st = (cudaStream_t)cuda_stream;
-  k_window_stats<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(d_ts, L, (int)window, d_means,
-                                                              nullptr, d_stds, nullptr);
+  launch_window_stats(d_ts, L, (int)window, d_means, nullptr, d_stds, nullptr, st);
   MPG_CUDA(cudaGetLastError());
   return MPGPU_OK;
 }
@@ -1418,8 +1427,7 @@ mpgpu_status mpgpu_distance_profiles(const double* d_ts, int64_t n, int64_t wind
   double* inv = mu + L;
   double* qstat = inv + L;
   double* stage = qstat + 3 * n_queries;
-  k_window_stats<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(d_ts, L, (int)window, mu, inv,
-                                                              nullptr, nullptr);
+  launch_window_stats(d_ts, L, (int)window, mu, inv, nullptr, nullptr, st);
   k_query_stats<<<(unsigned)((n_queries + kQStatWarps - 1) / kQStatWarps), kQStatWarps * 32, 0, st>>>(
       d_ts, d_queries, (const long long*)d_query_pos, (int)n_queries, (int)window, qstat);
   const unsigned gx = (unsigned)((L + kMassTile - 1) / kMassTile);
