@@ -62,3 +62,25 @@ def test_reversal_property(mp):
     rmu, rsd = _gpu_stats(mp, x[::-1].copy(), 100)
     assert np.allclose(rmu[::-1], mu, rtol=1e-12, atol=1e-12)
     assert np.allclose(rsd[::-1], sd, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("w", [4, 5, 100, 256, 513, 1000, 2049])
+def test_blocked_and_per_window_kernels_agree_bit_for_bit(mp, w):
+    """K1 switches kernels by series length (one thread per window below 303K
+    windows, 8 windows per thread on a register window above). Both add each
+    window's samples in order, so a long series and a slice of it give the
+    same bits for the windows they share (also across the 512-sample chunks of
+    the blocked kernel and for windows that are no multiple of 8 long)."""
+    import torch
+    g = np.random.default_rng(w)
+    n = 400_000 + w
+    x = np.cumsum(g.standard_normal(n)) * 1e3 + 1e6
+    x[1000:1000 + 3 * w] = x[1000]  # a flat run
+    xd = torch.from_numpy(x).cuda()
+    mu_l, sd_l = mp.rolling_stats(xd, w)                      # 400,001 windows: blocked
+    lo, cnt = 123_457, 50_000
+    mu_s, sd_s = mp.rolling_stats(xd[lo:lo + cnt + w - 1].contiguous(), w)   # 50,000 windows: per window
+    assert torch.equal(mu_l[lo:lo + cnt], mu_s) and torch.equal(sd_l[lo:lo + cnt], sd_s)
+    mu_h, sd_h = mp.rolling_stats(xd[:60_000 + w - 1].contiguous(), w)
+    assert torch.equal(mu_l[:60_000], mu_h) and torch.equal(sd_l[:60_000], sd_h)
+    assert float(sd_l[1000]) == 0.0
