@@ -70,3 +70,40 @@ def test_mass_row_equals_join_minimum(mp):
         j = int(np.argmin(out[k]))
         assert abs(out[k][j] - prof.values[p]) <= 1e-9 * max(1.0, prof.values[p])
         assert j == prof.index[p]
+
+
+def test_constant_memory_and_shared_memory_query_paths_agree(mp, tmp_path):
+    """k_mass<true> (queries as constant-bank operands, several launches when
+    they do not fit one) against k_mass<false> (queries staged in shared
+    memory; MPGPU_MASS_CONST=0, read once per process, hence the child): the
+    same sums in the same order, so the same bits. 70 queries of 300 samples
+    take three constant-memory launches; a 7,200-sample window exceeds the
+    constant buffer and runs the shared-memory form in this process too."""
+    import os
+    import subprocess
+    import sys
+    import torch
+    g = np.random.default_rng(5)
+    x = np.cumsum(g.standard_normal(60000))
+    x[700:1400] = x[700]
+    w, zone = 300, 150
+    pos = np.sort(g.choice(x.size - w, size=70, replace=False)).astype(np.int64)
+    pos[0] = 800  # a flat query
+    np.savez(tmp_path / "in.npz", x=x, pos=pos)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    child = (f"import sys, numpy as np, torch; sys.path.insert(0, {root!r}); import paper_1904_12626_b200 as mp; "
+             f"d = np.load({str(tmp_path / 'in.npz')!r}); "
+             f"o = mp.distance_profiles(torch.from_numpy(d['x']).cuda(), {w}, "
+             f"positions=torch.from_numpy(d['pos']).cuda(), zone={zone}); "
+             f"np.save({str(tmp_path / 'shared.npy')!r}, o.cpu().numpy())")
+    subprocess.run([sys.executable, "-c", child], check=True, timeout=600,
+                   env=dict(os.environ, MPGPU_MASS_CONST="0"))
+    out = mp.distance_profiles(torch.from_numpy(x).cuda(), w, positions=torch.from_numpy(pos).cuda(),
+                               zone=zone).cpu().numpy()
+    assert np.array_equal(out, np.load(tmp_path / "shared.npy"))
+    # a window longer than the constant buffer
+    wl = 7200
+    y = np.cumsum(g.standard_normal(3 * wl))
+    q = torch.from_numpy(np.array([0, wl // 2], dtype=np.int64)).cuda()
+    o = mp.distance_profiles(torch.from_numpy(y).cuda(), wl, positions=q, zone=-1).cpu().numpy()
+    assert o[0, 0] == 0.0 and o[1, wl // 2] == 0.0 and np.all(np.isfinite(o))
