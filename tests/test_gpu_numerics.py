@@ -82,3 +82,36 @@ def test_ab_anticorrelated(mp, oracle_lib):
     y = -x[:3000] + 1e-3 * np.random.default_rng(4).standard_normal(3000)
     got = _check(mp, oracle_lib, x, 50, y=y)
     assert np.all(got.index >= 0) and np.all(np.isfinite(got.values))
+
+
+@pytest.mark.parametrize("scale,offset", [(1.0, 1e8), (1e30, 0.0), (1e-6, 0.0)])
+def test_masked_anytime_on_hostile_scales(mp, scale, offset):
+    """The masked band join (exact anytime SCRIMP on a dense diagonal set) marks
+    the diagonals outside the set with a negative NaN covariance; neither a
+    huge offset nor extreme scales may turn that into a candidate or hide one.
+    Reference: direct z-normalised distances over the chosen diagonals in numpy
+    (the oracle's SCRIMP uses the raw-QT recurrence, which loses the signal to a
+    1e8 offset itself)."""
+    n, w, ez, seed = 4000, 64, 0.5, 17
+    x = _walk(n, 23) * scale + offset
+    L = n - w + 1
+    zone = mp.zone_size(w, ez)
+    s_size = (L - zone - 1) // 3
+    r = mp.scrimp(x, w, ez, s_size=s_size, seed=seed)
+    diags, _ = mp.scrimp_diagonals(n, w, zone, s_size, seed)
+    W = np.lib.stride_tricks.sliding_window_view(x, w)
+    Z = W - W.mean(axis=1, keepdims=True)
+    Z = Z / np.sqrt((Z * Z).sum(axis=1, keepdims=True) / w)  # unit population variance
+    ref = np.full(L, np.inf)
+    for k in diags:
+        k = int(k)
+        d = np.sqrt(np.maximum(((Z[:L - k] - Z[k:]) ** 2).sum(axis=1), 0.0))
+        ref[:L - k] = np.minimum(ref[:L - k], d)
+        ref[k:] = np.minimum(ref[k:], d)
+    ok, rel = close(r.values, ref)
+    assert ok, f"masked anytime at scale {scale:g} offset {offset:g}: max rel {rel:.3e}"
+    fin = r.index >= 0
+    assert fin.all() and np.isin(np.abs(r.index - np.arange(L)), diags).all()
+    # the reported neighbour attains the reported value
+    dd = np.sqrt(((Z - Z[r.index]) ** 2).sum(axis=1))
+    assert close(r.values, dd)[0]
